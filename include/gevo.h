@@ -1,0 +1,131 @@
+/* gevo.h -- C ABI of libgevo, the B200 fitness evaluator for GEVO-ML.
+ *
+ * The reference evaluates one patched program at a time on the CPU through
+ * Python objects.  libgevo evaluates a whole generation per call.  Each
+ * entry point names the reference interface it replaces:
+ *
+ *   gevo_create / gevo_destroy   -- (no reference analogue: owns a device,
+ *                                   a stream and all device memory)
+ *   gevo_upload_split            -- SplitView.whole_batches
+ *                                   (pkg/src/evotir/datasets.py:149-162),
+ *                                   uploaded once instead of per evaluation
+ *   gevo_upload_weights          -- module.constants[w1,b1,w2,b2]
+ *                                   (fitness.py:341, fitness.py:388)
+ *   gevo_eval                    -- evaluate() for a list of variants
+ *                                   (fitness.py:372-393, holdout_report
+ *                                   fitness.py:396-426), i.e. the body of
+ *                                   _Evaluator.__call__ (search.py:257-273)
+ *   gevo_exec_once               -- ExecPlan.run on explicit inputs
+ *                                   (interpreter.py:219-225, eval_op :272)
+ *   gevo_nsga2_rank              -- rank_population (search.py:143-150):
+ *                                   nondominated_sort :96-120 +
+ *                                   crowding_distance :123-140
+ *   gevo_nsga2_select            -- select_survivors (search.py:163-179)
+ *   gevo_last_error              -- (Python exceptions in the reference)
+ *   gevo_last_kernel_ms          -- (no analogue: device time of the last
+ *                                   gevo_eval launch, CUDA events on the
+ *                                   context's stream)
+ *
+ * Conventions: every call returns 0 on success and a negative GEVO_E_* code
+ * on failure (then gevo_last_error explains); no C++ exception crosses the
+ * ABI.  The caller owns host buffers; the context owns device memory.  One
+ * context per device, used by one host thread at a time.  Results are
+ * deterministic: no floating-point atomics anywhere.
+ * The launch-plan format consumed by gevo_eval is in gevo_plan.h.
+ */
+#ifndef GEVO_H
+#define GEVO_H
+#include <stddef.h>
+#include <stdint.h>
+#include "gevo_plan.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gevo_ctx gevo_ctx;
+
+enum {
+  GEVO_OK = 0,
+  GEVO_E_ARG = -1,      /* bad argument / malformed plan */
+  GEVO_E_CUDA = -2,     /* CUDA runtime failure */
+  GEVO_E_NOSPLIT = -3,  /* split id not uploaded */
+  GEVO_E_STATE = -4     /* weights not uploaded, ... */
+};
+
+/* per-individual status: the reference's failure encodings (fitness.py:
+ * 347-351 blow-up -> error 1.0; 364-365 non-finite probabilities -> 1.0) */
+enum {
+  GEVO_STATUS_OK = 0,
+  GEVO_STATUS_NONFINITE_WEIGHTS = 1,
+  GEVO_STATUS_NONFINITE_PROBS = 2,
+  GEVO_STATUS_EXEC_ERROR = 3
+};
+
+enum { GEVO_MODE_TRAIN = 0, GEVO_MODE_PREDICT = 1 };
+
+typedef struct {
+  int64_t wrong;      /* misclassified examples (0 unless status OK) */
+  int64_t total;      /* scored examples (0 unless status OK) */
+  int32_t status;     /* GEVO_STATUS_* */
+  int32_t steps_run;  /* training steps executed before an early exit */
+} gevo_result;
+
+typedef struct {
+  int32_t mode;          /* GEVO_MODE_TRAIN | GEVO_MODE_PREDICT */
+  int32_t steps;         /* WorkloadConfig.steps (fitness.py:61) */
+  int32_t check_every;   /* WorkloadConfig.finite_check_every */
+  int32_t train_split;   /* split whose batches train (search) */
+  int32_t score_split;   /* split scored by @forward (search or holdout) */
+  int32_t want_weights;  /* copy final weights out (n_ind * weight_elems) */
+} gevo_eval_desc;
+
+int gevo_create(int device, gevo_ctx** out);
+int gevo_destroy(gevo_ctx* ctx);
+const char* gevo_last_error(gevo_ctx* ctx);
+
+/* x: n x features row-major float64; labels: n int64.  Keeps the whole
+ * batches (partial trailing batch dropped) with one-hot targets. */
+int gevo_upload_split(gevo_ctx* ctx, int split_id, const double* x, int64_t n,
+                      int features, const int64_t* labels, int classes,
+                      int batch);
+
+/* concatenated initial (training) or frozen (prediction) weight arrays,
+ * C order, in @train_step return order */
+int gevo_upload_weights(gevo_ctx* ctx, const double* w, int64_t n_elems);
+
+int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
+              const gevo_eval_desc* desc, gevo_result* results,
+              double* final_weights);
+
+/* run prog.train0 once per prog: params from `params` (prog.param_off),
+ * returns into `outs` (prog.out_off); 64-bit words */
+int gevo_exec_once(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
+                   const double* params, size_t param_words, double* outs,
+                   size_t out_words);
+
+/* rank[i], crowding[i] for every point; front_of_order lists point indices
+ * front by front (front 0 in index order, later fronts ascending, as
+ * nondominated_sort returns them); front_start[f] indexes it (n_fronts+1
+ * entries).  Bit-exact with search.py:96-150. */
+int gevo_nsga2_rank(gevo_ctx* ctx, const double* cost, const double* error,
+                    int n, int32_t* rank, double* crowding,
+                    int32_t* front_order, int32_t* front_start,
+                    int32_t* n_fronts);
+
+/* indices chosen by select_survivors(pool, keep) in survivor order, plus the
+ * rank/crowding it assigns (search.py:163-179) */
+int gevo_nsga2_select(gevo_ctx* ctx, const double* cost, const double* error,
+                      int n, int keep, int32_t* chosen, int32_t* rank,
+                      double* crowding);
+
+/* device milliseconds of the evaluation kernel of the last gevo_eval */
+int gevo_last_kernel_ms(gevo_ctx* ctx, double* ms);
+
+/* device and build info, e.g. "NVIDIA B200 sm_100 148 SMs" */
+int gevo_device_info(gevo_ctx* ctx, char* buf, size_t len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

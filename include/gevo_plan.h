@@ -1,0 +1,101 @@
+/* gevo_plan.h -- the launch-plan format the host lowering hands to libgevo.
+ *
+ * A plan is one flat blob per generation:
+ *   gevo_plan_header | gevo_instr[n_instr] | gevo_prog[n_prog] | double consts[n_const]
+ * Each gevo_prog is one individual (one mutated program): index ranges into
+ * the instruction table for its @train_step (step 0 / steps >= 1, which can
+ * differ only in operand layouts) and its @forward, plus its arena size.
+ *
+ * Every device element is one 64-bit word (f32 of the dialect is computed as
+ * float64 exactly like the reference, ir.py:33-37; i32 -> int64; i1 -> int64
+ * 0/1).  Operands address a buffer (see GEVO_BUF_*) at an element offset with
+ * per-dimension element strides; views (transpose, broadcast_in_dim, slice,
+ * view-reshape) never become instructions -- they are folded into strides,
+ * exactly the numpy views the reference interpreter passes around
+ * (interpreter.py:118-153).
+ */
+#ifndef GEVO_PLAN_H
+#define GEVO_PLAN_H
+#include <stdint.h>
+
+#define GEVO_PLAN_MAGIC 0x47455650u /* "GEVP" */
+#define GEVO_PLAN_VERSION 1
+#define GEVO_MAXR 6        /* max tensor rank */
+#define GEVO_MAXP 8        /* max function params / returns */
+
+/* buffer ids */
+enum {
+  GEVO_BUF_ARENA = 0,               /* per-individual scratch */
+  GEVO_BUF_CONST = 1,               /* per-individual constant pool */
+  GEVO_BUF_PARAM0 = 2,              /* params 0..7 -> ids 2..9 */
+  GEVO_BUF_OUT0 = 2 + GEVO_MAXP,    /* returns 0..7 -> ids 10..17 */
+  GEVO_NBUF = 2 + 2 * GEVO_MAXP
+};
+
+/* element kinds */
+enum { GEVO_K_F64 = 0, GEVO_K_I64 = 1, GEVO_K_I1 = 2 };
+
+/* instruction classes (interpreter.py:78-185) */
+enum {
+  GEVO_OP_UNARY = 1,   /* sub: GEVO_U_* */
+  GEVO_OP_BINARY = 2,  /* sub: GEVO_B_* */
+  GEVO_OP_SELECT = 3,
+  GEVO_OP_REDUCE = 4,  /* sub: GEVO_R_*; aux[0]=L, aux[1]=stride along axis */
+  GEVO_OP_DOT = 5,     /* sub: GEVO_D_* for columns < aux[1]; aux[2] for the
+                          rest; aux[0]=K */
+  GEVO_OP_PAD = 6      /* aux[d]=low[d], aux2[d]=input extent[d] */
+};
+enum { GEVO_U_NEG = 0, GEVO_U_EXP, GEVO_U_LOG, GEVO_U_COPY, GEVO_U_CVT };
+enum {
+  GEVO_B_ADD = 0, GEVO_B_SUB, GEVO_B_MUL, GEVO_B_DIV, GEVO_B_MAX,
+  GEVO_B_EQ, GEVO_B_NE, GEVO_B_LT, GEVO_B_LE, GEVO_B_GT, GEVO_B_GE
+};
+/* summation orders reproduced from numpy */
+enum { GEVO_R_SUM_PAIRWISE = 0, GEVO_R_SUM_SEQ = 1, GEVO_R_MAX = 2 };
+enum {
+  GEVO_D_FMA_CHAIN = 0,   /* acc = fma(a_k, b_k, acc), k ascending, acc0 = 0 */
+  GEVO_D_ACC8_TREE = 1,   /* 8 lane accumulators (k mod 8), pairwise tree */
+  GEVO_D_SEQ_NOFMA = 2,   /* numpy's own loop: acc += a_k * b_k (rounded) */
+  GEVO_D_ACC8_TAIL = 3    /* 8 lanes over k < K&~7, tree, then fma tail */
+};
+
+typedef struct {
+  int32_t buf;
+  int32_t off;
+  int32_t st[GEVO_MAXR];
+} gevo_operand;                       /* 32 bytes */
+
+typedef struct {
+  int32_t op, sub, kout, kin;
+  int32_t rank, n;                    /* output rank, element count */
+  int32_t shp[GEVO_MAXR];             /* output shape */
+  int32_t aux[GEVO_MAXR];
+  int32_t aux2[GEVO_MAXR];
+  gevo_operand out;                   /* out.st: the numpy layout of the result */
+  gevo_operand in[3];
+} gevo_instr;                         /* 224 bytes */
+
+typedef struct {
+  int32_t train0, train0_n;           /* @train_step, step 0 */
+  int32_t train1, train1_n;           /* @train_step, steps >= 1 */
+  int32_t fwd, fwd_n;                 /* @forward */
+  int32_t const_off;                  /* element offset into the const pool */
+  int32_t result_slot;                /* where this individual's result goes */
+  int64_t arena_off;                  /* element offset of [arena|w0|w1] */
+  int32_t arena_elems;                /* scratch elements (before weights) */
+  int32_t flags;
+  int32_t param_off[GEVO_MAXP];       /* exec-once: offsets into params blob */
+  int32_t out_off[GEVO_MAXP];         /* exec-once: offsets into outs blob */
+} gevo_prog;                          /* 112 bytes */
+
+typedef struct {
+  uint32_t magic, version;
+  int32_t n_instr, n_prog, n_const;
+  int32_t weight_elems;               /* per-individual weight block */
+  int32_t n_weights;                  /* weight arrays (returns of train_step) */
+  int32_t wofs[GEVO_MAXP];            /* offsets of each weight in the block */
+  int32_t max_arena;                  /* largest arena_elems of any prog */
+  int64_t total_elems;                /* device elements for all individuals */
+} gevo_plan_header;
+
+#endif

@@ -1,0 +1,424 @@
+// gevo_abi.cu -- the C ABI of libgevo (declared in include/gevo.h).
+//
+// Owns the device, one stream, the resident dataset splits, the shared
+// initial weights and the growable device arena; validates plans; no C++
+// exception crosses the boundary.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+#include <string>
+#include <vector>
+#include "gevo.h"
+#include "gevo_exec.cuh"
+
+using namespace gevo;
+
+namespace {
+
+struct Split {
+  double* x = nullptr;         // [nb, B, F]
+  double* y = nullptr;         // [nb, B, C] one-hot
+  int64_t* labels = nullptr;   // [nb, B]
+  int nb = 0, batch = 0, features = 0, classes = 0;
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes + bytes / 4 + 256;
+    if (cudaMalloc(&p, want) != cudaSuccess) return -1;
+    cap = want;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct gevo_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  Split splits[4];
+  double* weights = nullptr;
+  int64_t weight_elems = 0;
+  DevBuf plan, arena, results, finalw, params, outs, ns;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;
+};
+
+static int fail(gevo_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+static int cuda_fail(gevo_ctx* c, cudaError_t e, const char* what) {
+  return fail(c, GEVO_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                              \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr);  \
+  } while (0)
+
+namespace {
+
+struct PlanView {
+  const gevo_plan_header* h;
+  size_t instr_off, prog_off, const_off;
+};
+
+int parse_plan(gevo_ctx* ctx, const void* plan, size_t bytes, PlanView* v) {
+  if (!plan || bytes < sizeof(gevo_plan_header))
+    return fail(ctx, GEVO_E_ARG, "plan blob too small");
+  const gevo_plan_header* h = static_cast<const gevo_plan_header*>(plan);
+  if (h->magic != GEVO_PLAN_MAGIC || h->version != GEVO_PLAN_VERSION)
+    return fail(ctx, GEVO_E_ARG, "bad plan magic/version");
+  if (h->n_instr < 0 || h->n_prog < 0 || h->n_const < 0 || h->total_elems < 0)
+    return fail(ctx, GEVO_E_ARG, "negative plan counts");
+  size_t need = sizeof(gevo_plan_header) + (size_t)h->n_instr * sizeof(gevo_instr) +
+                (size_t)h->n_prog * sizeof(gevo_prog) + (size_t)h->n_const * 8;
+  if (need != bytes) return fail(ctx, GEVO_E_ARG, "plan size mismatch");
+  v->h = h;
+  v->instr_off = sizeof(gevo_plan_header);
+  v->prog_off = v->instr_off + (size_t)h->n_instr * sizeof(gevo_instr);
+  v->const_off = v->prog_off + (size_t)h->n_prog * sizeof(gevo_prog);
+  // host-side validation of every instruction range
+  const gevo_prog* progs = reinterpret_cast<const gevo_prog*>(
+      static_cast<const char*>(plan) + v->prog_off);
+  for (int i = 0; i < h->n_prog; ++i) {
+    const gevo_prog& p = progs[i];
+    auto ok = [&](int o, int n) { return o >= 0 && n >= 0 && o + n <= h->n_instr; };
+    if (!ok(p.train0, p.train0_n) || !ok(p.train1, p.train1_n) || !ok(p.fwd, p.fwd_n))
+      return fail(ctx, GEVO_E_ARG, "prog instruction range out of bounds");
+    if (p.arena_off < 0 || p.arena_off > h->total_elems)
+      return fail(ctx, GEVO_E_ARG, "prog arena offset out of bounds");
+  }
+  return 0;
+}
+
+int upload_plan(gevo_ctx* ctx, const void* plan, size_t bytes, const PlanView& v,
+                const gevo_instr** di, const gevo_prog** dp, const double** dc) {
+  if (ctx->plan.ensure(bytes + 16)) return fail(ctx, GEVO_E_CUDA, "plan alloc failed");
+  CK(cudaMemcpyAsync(ctx->plan.p, plan, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  char* base = static_cast<char*>(ctx->plan.p);
+  *di = reinterpret_cast<const gevo_instr*>(base + v.instr_off);
+  *dp = reinterpret_cast<const gevo_prog*>(base + v.prog_off);
+  *dc = reinterpret_cast<const double*>(base + v.const_off);
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gevo_create(int device, gevo_ctx** out) {
+  if (!out) return GEVO_E_ARG;
+  *out = nullptr;
+  gevo_ctx* ctx = new (std::nothrow) gevo_ctx();
+  if (!ctx) return GEVO_E_ARG;
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
+  if (e != cudaSuccess) {
+    // keep the context so the caller can read the error
+    ctx->err = std::string("cuda init: ") + cudaGetErrorString(e);
+    *out = ctx;
+    return GEVO_E_CUDA;
+  }
+  *out = ctx;
+  return GEVO_OK;
+}
+
+int gevo_destroy(gevo_ctx* ctx) {
+  if (!ctx) return GEVO_E_ARG;
+  cudaSetDevice(ctx->device);
+  for (auto& s : ctx->splits) {
+    cudaFree(s.x);
+    cudaFree(s.y);
+    cudaFree(s.labels);
+  }
+  cudaFree(ctx->weights);
+  ctx->plan.release();
+  ctx->arena.release();
+  ctx->results.release();
+  ctx->finalw.release();
+  ctx->params.release();
+  ctx->outs.release();
+  ctx->ns.release();
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return GEVO_OK;
+}
+
+const char* gevo_last_error(gevo_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : "null context";
+}
+
+int gevo_device_info(gevo_ctx* ctx, char* buf, size_t len) {
+  if (!ctx || !buf || !len) return GEVO_E_ARG;
+  cudaDeviceProp p;
+  CK(cudaGetDeviceProperties(&p, ctx->device));
+  snprintf(buf, len, "%s sm_%d%d %d SMs", p.name, p.major, p.minor, p.multiProcessorCount);
+  return GEVO_OK;
+}
+
+int gevo_upload_split(gevo_ctx* ctx, int split_id, const double* x, int64_t n,
+                      int features, const int64_t* labels, int classes, int batch) {
+  if (!ctx) return GEVO_E_ARG;
+  if (split_id < 0 || split_id >= 4 || !x || !labels || n < 0 || features <= 0 ||
+      classes <= 0 || batch <= 0)
+    return fail(ctx, GEVO_E_ARG, "bad split arguments");
+  CK(cudaSetDevice(ctx->device));
+  Split& s = ctx->splits[split_id];
+  cudaFree(s.x);
+  cudaFree(s.y);
+  cudaFree(s.labels);
+  s = Split();
+  const int nb = (int)(n / batch);
+  const int64_t rows = (int64_t)nb * batch;
+  for (int64_t i = 0; i < rows; ++i)
+    if (labels[i] < 0 || labels[i] >= classes)
+      return fail(ctx, GEVO_E_ARG, "label out of range");
+  std::vector<double> y((size_t)rows * classes, 0.0);
+  for (int64_t i = 0; i < rows; ++i) y[(size_t)i * classes + labels[i]] = 1.0;
+  if (rows > 0) {
+    CK(cudaMalloc(&s.x, rows * features * sizeof(double)));
+    CK(cudaMalloc(&s.y, rows * classes * sizeof(double)));
+    CK(cudaMalloc(&s.labels, rows * sizeof(int64_t)));
+    CK(cudaMemcpy(s.x, x, rows * features * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(s.y, y.data(), rows * classes * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(s.labels, labels, rows * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  s.nb = nb;
+  s.batch = batch;
+  s.features = features;
+  s.classes = classes;
+  return GEVO_OK;
+}
+
+int gevo_upload_weights(gevo_ctx* ctx, const double* w, int64_t n_elems) {
+  if (!ctx) return GEVO_E_ARG;
+  if (!w || n_elems <= 0) return fail(ctx, GEVO_E_ARG, "bad weights");
+  CK(cudaSetDevice(ctx->device));
+  cudaFree(ctx->weights);
+  ctx->weights = nullptr;
+  CK(cudaMalloc(&ctx->weights, n_elems * sizeof(double)));
+  CK(cudaMemcpy(ctx->weights, w, n_elems * sizeof(double), cudaMemcpyHostToDevice));
+  ctx->weight_elems = n_elems;
+  return GEVO_OK;
+}
+
+int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
+              const gevo_eval_desc* desc, gevo_result* results, double* final_weights) {
+  if (!ctx) return GEVO_E_ARG;
+  if (!desc || !results) return fail(ctx, GEVO_E_ARG, "null desc/results");
+  CK(cudaSetDevice(ctx->device));
+  PlanView v;
+  int rc = parse_plan(ctx, plan, plan_bytes, &v);
+  if (rc) return rc;
+  const gevo_plan_header* h = v.h;
+  if (h->n_prog == 0) return GEVO_OK;
+  if (!ctx->weights) return fail(ctx, GEVO_E_STATE, "weights not uploaded");
+  if (h->weight_elems != ctx->weight_elems)
+    return fail(ctx, GEVO_E_ARG, "plan weight block does not match uploaded weights");
+  if (desc->score_split < 0 || desc->score_split >= 4 || !ctx->splits[desc->score_split].x)
+    return fail(ctx, GEVO_E_NOSPLIT, "score split not uploaded");
+  const Split& sc = ctx->splits[desc->score_split];
+  const Split* tr = nullptr;
+  if (desc->mode == GEVO_MODE_TRAIN) {
+    if (desc->train_split < 0 || desc->train_split >= 4 || !ctx->splits[desc->train_split].x)
+      return fail(ctx, GEVO_E_NOSPLIT, "train split not uploaded");
+    tr = &ctx->splits[desc->train_split];
+    if (tr->batch != sc.batch || tr->features != sc.features || tr->classes != sc.classes)
+      return fail(ctx, GEVO_E_ARG, "train/score split shapes differ");
+    if (desc->steps < 0) return fail(ctx, GEVO_E_ARG, "negative steps");
+  } else if (desc->mode != GEVO_MODE_PREDICT) {
+    return fail(ctx, GEVO_E_ARG, "bad mode");
+  }
+  if (h->n_weights < 0 || h->n_weights > GEVO_MAXP - 2)
+    return fail(ctx, GEVO_E_ARG, "bad weight count");
+
+  const gevo_instr* di;
+  const gevo_prog* dp;
+  const double* dc;
+  rc = upload_plan(ctx, plan, plan_bytes, v, &di, &dp, &dc);
+  if (rc) return rc;
+  if (ctx->arena.ensure((size_t)h->total_elems * sizeof(double) + 64))
+    return fail(ctx, GEVO_E_CUDA, "arena alloc failed");
+  if (ctx->results.ensure((size_t)h->n_prog * sizeof(gevo_result)))
+    return fail(ctx, GEVO_E_CUDA, "results alloc failed");
+  if (final_weights &&
+      ctx->finalw.ensure((size_t)h->n_prog * h->weight_elems * sizeof(double) + 8))
+    return fail(ctx, GEVO_E_CUDA, "final weight alloc failed");
+
+  EvalArgs a;
+  memset(&a, 0, sizeof(a));
+  a.instrs = di;
+  a.progs = dp;
+  a.consts = dc;
+  a.arena = static_cast<double*>(ctx->arena.p);
+  for (int i = 0; i < GEVO_MAXP; ++i) a.wofs[i] = h->wofs[i];
+  a.n_weights = h->n_weights;
+  a.weight_elems = h->weight_elems;
+  a.probs_elems = sc.batch * sc.classes;
+  a.mode = desc->mode;
+  a.steps = desc->steps;
+  a.check_every = desc->check_every;
+  a.init_weights = ctx->weights;
+  if (tr) {
+    a.train_x = tr->x;
+    a.train_y = tr->y;
+    a.train_nb = tr->nb;
+  }
+  a.score_x = sc.x;
+  a.score_labels = sc.labels;
+  a.score_nb = sc.nb;
+  a.batch = sc.batch;
+  a.classes = sc.classes;
+  a.x_elems = (int64_t)sc.batch * sc.features;
+  a.y_elems = (int64_t)sc.batch * sc.classes;
+  a.results = static_cast<gevo_result*>(ctx->results.p);
+  a.final_weights = final_weights ? static_cast<double*>(ctx->finalw.p) : nullptr;
+  if (a.mode == GEVO_MODE_TRAIN && a.train_nb == 0 && a.steps > 0)
+    return fail(ctx, GEVO_E_ARG, "train split has no whole batch");
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  launch_eval(a, h->n_prog, ctx->stream);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  CK(cudaMemcpyAsync(results, ctx->results.p, (size_t)h->n_prog * sizeof(gevo_result),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  if (final_weights)
+    CK(cudaMemcpyAsync(final_weights, ctx->finalw.p,
+                       (size_t)h->n_prog * h->weight_elems * sizeof(double),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  ctx->last_ms = ms;
+  return GEVO_OK;
+}
+
+int gevo_last_kernel_ms(gevo_ctx* ctx, double* ms) {
+  if (!ctx || !ms) return GEVO_E_ARG;
+  *ms = ctx->last_ms;
+  return GEVO_OK;
+}
+
+int gevo_exec_once(gevo_ctx* ctx, const void* plan, size_t plan_bytes, const double* params,
+                   size_t param_words, double* outs, size_t out_words) {
+  if (!ctx) return GEVO_E_ARG;
+  if (!params || !outs) return fail(ctx, GEVO_E_ARG, "null params/outs");
+  CK(cudaSetDevice(ctx->device));
+  PlanView v;
+  int rc = parse_plan(ctx, plan, plan_bytes, &v);
+  if (rc) return rc;
+  const gevo_plan_header* h = v.h;
+  if (h->n_prog == 0) return GEVO_OK;
+  const gevo_instr* di;
+  const gevo_prog* dp;
+  const double* dc;
+  rc = upload_plan(ctx, plan, plan_bytes, v, &di, &dp, &dc);
+  if (rc) return rc;
+  if (ctx->arena.ensure((size_t)h->total_elems * sizeof(double) + 64) ||
+      ctx->params.ensure(param_words * 8 + 8) || ctx->outs.ensure(out_words * 8 + 8))
+    return fail(ctx, GEVO_E_CUDA, "exec-once alloc failed");
+  CK(cudaMemcpyAsync(ctx->params.p, params, param_words * 8, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemsetAsync(ctx->outs.p, 0, out_words * 8, ctx->stream));
+  OnceArgs a;
+  a.instrs = di;
+  a.progs = dp;
+  a.consts = dc;
+  a.arena = static_cast<double*>(ctx->arena.p);
+  a.params = static_cast<const double*>(ctx->params.p);
+  a.outs = static_cast<double*>(ctx->outs.p);
+  launch_once(a, h->n_prog, ctx->stream);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(outs, ctx->outs.p, out_words * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return GEVO_OK;
+}
+
+static int nsga2_common(gevo_ctx* ctx, const double* cost, const double* error, int n,
+                        int keep, int32_t* chosen, int32_t* rank, double* crowding,
+                        int32_t* front_order, int32_t* front_start, int32_t* n_fronts) {
+  if (!ctx) return GEVO_E_ARG;
+  if (n < 0 || !cost || !error) return fail(ctx, GEVO_E_ARG, "bad nsga2 arguments");
+  if (n == 0) {
+    if (n_fronts) *n_fronts = 0;
+    if (front_start) front_start[0] = 0;
+    return GEVO_OK;
+  }
+  CK(cudaSetDevice(ctx->device));
+  // layout: c[n] e[n] crowd[n] | rank order fstart(n+1) nf count ord0 ord1 fop chosen
+  size_t dbl = 3 * (size_t)n * 8;
+  size_t ints = (size_t)(8 * n + 2 + (keep > 0 ? keep : 0)) * 4;
+  if (ctx->ns.ensure(dbl + ints + 64)) return fail(ctx, GEVO_E_CUDA, "nsga2 alloc failed");
+  double* d = static_cast<double*>(ctx->ns.p);
+  int32_t* iv = reinterpret_cast<int32_t*>(d + 3 * (size_t)n);
+  NsArgs a;
+  a.n = n;
+  a.keep = keep;
+  a.c = d;
+  a.e = d + n;
+  a.crowd = d + 2 * (size_t)n;
+  a.rank = iv;
+  a.order = iv + n;
+  a.fstart = iv + 2 * n;
+  a.nfronts = iv + 3 * n + 1;
+  a.count = iv + 3 * n + 2;
+  a.ord0 = iv + 4 * n + 2;
+  a.ord1 = iv + 5 * n + 2;
+  a.front_of_pos = iv + 6 * n + 2;
+  a.chosen = chosen ? iv + 7 * n + 2 : nullptr;
+  CK(cudaMemcpyAsync(d, cost, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d + n, error, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  launch_nsga2(a, ctx->stream);
+  CK(cudaGetLastError());
+  int32_t nf = 0;
+  CK(cudaMemcpyAsync(&nf, a.nfronts, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (rank) CK(cudaMemcpyAsync(rank, a.rank, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (crowding)
+    CK(cudaMemcpyAsync(crowding, a.crowd, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (front_order)
+    CK(cudaMemcpyAsync(front_order, a.order, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (front_start)
+    CK(cudaMemcpy(front_start, a.fstart, (size_t)(nf + 1) * 4, cudaMemcpyDeviceToHost));
+  if (chosen && keep > 0)
+    CK(cudaMemcpy(chosen, a.chosen, (size_t)keep * 4, cudaMemcpyDeviceToHost));
+  if (n_fronts) *n_fronts = nf;
+  return GEVO_OK;
+}
+
+int gevo_nsga2_rank(gevo_ctx* ctx, const double* cost, const double* error, int n,
+                    int32_t* rank, double* crowding, int32_t* front_order,
+                    int32_t* front_start, int32_t* n_fronts) {
+  return nsga2_common(ctx, cost, error, n, 0, nullptr, rank, crowding, front_order,
+                      front_start, n_fronts);
+}
+
+int gevo_nsga2_select(gevo_ctx* ctx, const double* cost, const double* error, int n,
+                      int keep, int32_t* chosen, int32_t* rank, double* crowding) {
+  if (keep < 0 || keep > n) return fail(ctx, GEVO_E_ARG, "keep out of range");
+  return nsga2_common(ctx, cost, error, n, keep, chosen, rank, crowding, nullptr, nullptr,
+                      nullptr);
+}
+
+}  // extern "C"

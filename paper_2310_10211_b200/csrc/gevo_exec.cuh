@@ -1,0 +1,60 @@
+// gevo_exec.cuh -- internal launch interfaces of the executor.
+#pragma once
+#include <cuda_runtime.h>
+#include "gevo.h"
+
+namespace gevo {
+
+struct EvalArgs {
+  const gevo_instr* instrs;
+  const gevo_prog* progs;
+  const double* consts;
+  double* arena;
+  int32_t wofs[GEVO_MAXP];
+  int n_weights, weight_elems, probs_elems;
+  int mode, steps, check_every;
+  const double* init_weights;
+  const double* train_x;
+  const double* train_y;
+  int train_nb;
+  const double* score_x;
+  const int64_t* score_labels;
+  int score_nb;
+  int batch, classes;
+  int64_t x_elems, y_elems;   // per batch
+  gevo_result* results;
+  double* final_weights;      // nullable
+};
+
+struct OnceArgs {
+  const gevo_instr* instrs;
+  const gevo_prog* progs;
+  const double* consts;
+  double* arena;
+  const double* params;
+  double* outs;
+};
+
+void launch_eval(const EvalArgs& a, int n_prog, cudaStream_t st);
+void launch_once(const OnceArgs& a, int n_prog, cudaStream_t st);
+
+// NSGA-II (nsga2.cu)
+struct NsArgs {
+  int n, keep;
+  const double* c;
+  const double* e;
+  int32_t* rank;      // [n]
+  double* crowd;      // [n]
+  int32_t* order;     // [n] points grouped by front
+  int32_t* fstart;    // [n+1]
+  int32_t* nfronts;   // [1]
+  int32_t* chosen;    // [keep] or null
+  int32_t* count;     // scratch [n]
+  int32_t* ord0;      // scratch [n] front-local order along axis 0
+  int32_t* ord1;      // scratch [n] front-local order along axis 1
+  int32_t* front_of_pos;  // scratch [n]
+};
+
+void launch_nsga2(const NsArgs& a, cudaStream_t st);
+
+}  // namespace gevo

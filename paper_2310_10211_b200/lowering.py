@@ -1,0 +1,492 @@
+"""Lowering: variant function -> device launch plan (include/gevo_plan.h).
+
+Replaces the reference's per-individual `ExecPlan` compile
+(interpreter.py:188-217) with a pass that emits one instruction table per
+function for the device executor.  Per op:
+
+  constant / iota             -> constant pool (no instruction)
+  transpose, broadcast_in_dim,
+  slice, view-reshape         -> folded into operand strides (no instruction)
+  copy-reshape                -> UNARY COPY into C order (numpy copies too)
+  elementwise / compare /
+  select / convert            -> UNARY / BINARY / SELECT
+  reduce                      -> REDUCE with numpy's summation order
+  dot                         -> DOT with numpy/OpenBLAS's summation order
+  pad                         -> PAD
+
+Results are stored in the memory order numpy would allocate them in
+(layout.py), scratch is reused by liveness, and a returned value is written
+straight into its weight slot when possible (else copied there).  The static
+cost is the reference CostModel (interpreter.py:51-59) accumulated in op
+order, so it is bit-identical.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import layout as L
+from .dialect import kind_name
+
+# --- constants mirrored from include/gevo_plan.h ----------------------------
+MAXR, MAXP = 6, 8
+BUF_ARENA, BUF_CONST, BUF_PARAM0, BUF_OUT0 = 0, 1, 2, 2 + MAXP
+K_F64, K_I64, K_I1 = 0, 1, 2
+KIND = {"f32": K_F64, "i32": K_I64, "i1": K_I1}
+OP_UNARY, OP_BINARY, OP_SELECT, OP_REDUCE, OP_DOT, OP_PAD = 1, 2, 3, 4, 5, 6
+U_NEG, U_EXP, U_LOG, U_COPY, U_CVT = range(5)
+B_CODES = {"add": 0, "subtract": 1, "multiply": 2, "divide": 3, "maximum": 4}
+CMP_CODES = {"eq": 5, "ne": 6, "lt": 7, "le": 8, "gt": 9, "ge": 10}
+R_SUM_PAIRWISE, R_SUM_SEQ, R_MAX = 0, 1, 2
+D_FMA_CHAIN, D_ACC8_TREE, D_SEQ_NOFMA, D_ACC8_TAIL = 0, 1, 2, 3
+
+PLAN_MAGIC, PLAN_VERSION = 0x47455650, 1
+
+_OPERAND = [("buf", "<i4"), ("off", "<i4"), ("st", "<i4", (MAXR,))]
+INSTR_DTYPE = np.dtype([
+    ("op", "<i4"), ("sub", "<i4"), ("kout", "<i4"), ("kin", "<i4"),
+    ("rank", "<i4"), ("n", "<i4"), ("shp", "<i4", (MAXR,)),
+    ("aux", "<i4", (MAXR,)), ("aux2", "<i4", (MAXR,)),
+    ("out", _OPERAND), ("in", _OPERAND, (3,))], align=True)
+PROG_DTYPE = np.dtype([
+    ("train0", "<i4"), ("train0_n", "<i4"), ("train1", "<i4"),
+    ("train1_n", "<i4"), ("fwd", "<i4"), ("fwd_n", "<i4"),
+    ("const_off", "<i4"), ("result_slot", "<i4"), ("arena_off", "<i8"),
+    ("arena_elems", "<i4"), ("flags", "<i4"),
+    ("param_off", "<i4", (MAXP,)), ("out_off", "<i4", (MAXP,))], align=True)
+HEADER_DTYPE = np.dtype([
+    ("magic", "<u4"), ("version", "<u4"), ("n_instr", "<i4"),
+    ("n_prog", "<i4"), ("n_const", "<i4"), ("weight_elems", "<i4"),
+    ("n_weights", "<i4"), ("wofs", "<i4", (MAXP,)), ("max_arena", "<i4"),
+    ("total_elems", "<i8")], align=True)
+assert INSTR_DTYPE.itemsize == 224 and PROG_DTYPE.itemsize == 112
+assert HEADER_DTYPE.itemsize == 72
+
+FLAG_LAYOUT_APPROX = 1     # returned layouts did not reach a fixed point
+
+_NP_DTYPE = {K_F64: np.float64, K_I64: np.int64, K_I1: np.int64}
+
+
+class LoweringError(Exception):
+    pass
+
+
+@dataclass
+class Val:
+    buf: int
+    off: int
+    shape: tuple
+    st: tuple
+    kind: int
+    alloc: int = -1      # arena allocation id backing this value (-1: none)
+
+
+@dataclass
+class Lowered:
+    instrs: list
+    consts: list                 # float/int values (64-bit) in pool order
+    arena_elems: int
+    ret_strides: list            # numpy layout of each returned value
+    cost: float
+
+
+@dataclass
+class _Alloc:
+    size: int
+    off: int = -1
+    fixed: tuple | None = None   # (buf, off) when stored outside the arena
+
+
+def _kind_of(ty) -> int:
+    return KIND[kind_name(ty.kind)]
+
+
+def _blas2d(s_outer, s_inner, d_inner) -> bool:
+    # numpy is_blasable2d (element units): unit inner stride, outer >= inner dim
+    return s_inner == 1 and s_outer >= d_inner
+
+
+def dot_modes(a: Val, b: Val):
+    """(mode for columns < split, split, mode for the rest) reproducing the
+    summation order numpy `@` + OpenBLAS (SkylakeX kernels, the build
+    container's numpy 2.3 / OpenBLAS 0.3.30) use; see DESIGN.md."""
+    m, k = a.shape
+    n = b.shape[1]
+    if a.kind != K_F64:
+        return D_SEQ_NOFMA, n, D_SEQ_NOFMA       # integer: exact anyway
+    a_c = _blas2d(a.st[0], a.st[1], k)
+    a_f = _blas2d(a.st[1], a.st[0], m)
+    b_c = _blas2d(b.st[0], b.st[1], n)
+    b_f = _blas2d(b.st[1], b.st[0], k)
+    if not ((a_c or a_f) and (b_c or b_f)):
+        return D_SEQ_NOFMA, n, D_SEQ_NOFMA       # numpy's own loop
+    if m == 1 or k == 1 or n == 1:
+        return D_FMA_CHAIN, n, D_FMA_CHAIN       # gemv/dot paths (see DESIGN)
+    trans_a, trans_b = not a_c, not b_c
+    # cblas row-major -> col-major: A' = B (trans_b), B' = A (trans_a)
+    tn = trans_b and not trans_a
+    small = m * n * k <= 1_000_000 and (not tn or (m * n <= 1200 and k >= 32))
+    if small and tn:
+        return D_ACC8_TREE, n, D_ACC8_TREE
+    if not trans_a and not trans_b and n % 8:
+        return D_FMA_CHAIN, n - n % 8, D_ACC8_TREE
+    return D_FMA_CHAIN, n, D_FMA_CHAIN
+
+
+def _pad_dims(shape):
+    shape = tuple(shape)
+    return list(shape) + [1] * (MAXR - len(shape))
+
+
+class _Builder:
+    def __init__(self, fn, param_vals, ret_bufs, ret_layout, cost_table):
+        self.fn = fn
+        self.instrs = []
+        self.consts = []
+        self.allocs: list[_Alloc] = []
+        self.vals: dict[str, Val] = {}
+        self.cost = 0.0
+        self.table = cost_table or {}
+        self.ret_bufs = ret_bufs
+        self.ret_layout = ret_layout   # "compact" | "c"
+        types = {}
+        for (name, ty), v in zip(fn.params, param_vals):
+            self.vals[name] = v
+            types[name] = ty
+        self.types = types
+
+    # -- allocation ---------------------------------------------------------
+    def new_alloc(self, size, fixed=None) -> int:
+        self.allocs.append(_Alloc(size=size, fixed=fixed))
+        return len(self.allocs) - 1
+
+    def fresh(self, shape, st, kind, size, fixed=None) -> Val:
+        aid = self.new_alloc(size, fixed)
+        if fixed is not None:
+            return Val(fixed[0], fixed[1], tuple(shape), tuple(st), kind, aid)
+        return Val(BUF_ARENA, 0, tuple(shape), tuple(st), kind, aid)
+
+    def const(self, arr, kind) -> Val:
+        arr = np.asarray(arr)
+        off = len(self.consts)
+        flat = np.ascontiguousarray(arr).reshape(-1)
+        if kind == K_F64:
+            self.consts.extend(float(x) for x in flat)
+        else:
+            self.consts.extend(int(x) for x in flat)
+        return Val(BUF_CONST, off, tuple(arr.shape), L.c_strides(arr.shape), kind)
+
+    # -- instruction emission ------------------------------------------------
+    def operand(self, v: Val, shape_rank):
+        st = list(v.st) + [0] * (MAXR - len(v.st))
+        return (v.buf, v.off, st)
+
+    def emit(self, op, sub, out: Val, ins, kin=None, aux=None, aux2=None,
+             rank=None, shp=None, n=None):
+        shp = tuple(out.shape) if shp is None else tuple(shp)
+        rec = {
+            "op": op, "sub": sub, "kout": out.kind,
+            "kin": ins[0].kind if kin is None and ins else (kin or 0),
+            "rank": len(shp) if rank is None else rank,
+            "n": int(np.prod(shp, dtype=np.int64)) if n is None else n,
+            "shp": _pad_dims(shp), "aux": list(aux or []) + [0] * (MAXR - len(aux or [])),
+            "aux2": list(aux2 or []) + [0] * (MAXR - len(aux2 or [])),
+            "out": out, "in": list(ins)}
+        self.instrs.append(rec)
+
+    # -- lowering ---------------------------------------------------------------
+    def run(self, plan_returns):
+        fn = self.fn
+        # returned values produced by a materialising op go straight to OUT
+        direct = {}
+        for r, v in enumerate(fn.returns):
+            if v not in direct and r < len(self.ret_bufs):
+                direct[v] = r
+        self.direct = direct
+        for idx, op in enumerate(fn.ops):
+            tys = tuple(self.types[v] for v in op.operands)
+            self.cost += _op_cost(op, tys, self.table)
+            ins = [self.vals[v] for v in op.operands]
+            out = self.lower_op(op, ins, tys, idx)
+            self.vals[op.result] = out
+            self.types[op.result] = op.result_type
+        # returns
+        ret_st = []   # layout each return is STORED in (next step's params)
+        for r, name in enumerate(fn.returns):
+            v = self.vals[name]
+            if r >= len(self.ret_bufs):
+                ret_st.append(tuple(v.st))
+                continue
+            buf = self.ret_bufs[r]
+            if v.buf == buf[0] and v.off == buf[1] and direct.get(name) == r:
+                ret_st.append(tuple(v.st))
+                continue  # produced in place
+            st = self.ret_strides(v)
+            dst = Val(buf[0], buf[1], v.shape, st, v.kind)
+            self.emit(OP_UNARY, U_COPY, dst, [v])
+            ret_st.append(tuple(st))
+        return ret_st
+
+    def ret_strides(self, v: Val):
+        if self.ret_layout == "c":
+            return L.c_strides(v.shape)
+        return L.compact_strides(v.shape, v.st)[0]
+
+    def result_val(self, op, shape, st, kind):
+        """Storage for a materialised result: the OUT slot if it is returned
+        (and dense in numpy's layout), else a fresh arena allocation."""
+        r = self.direct.get(op.result)
+        count = int(np.prod(shape, dtype=np.int64)) if shape else 1
+        if r is not None and self.ret_layout == "c" and \
+                tuple(st) != L.c_strides(shape):
+            r = None
+        if r is not None:
+            return self.fresh(shape, st, kind, 0, fixed=self.ret_bufs[r])
+        return self.fresh(shape, st, kind, count)
+
+    def lower_op(self, op, ins, tys, idx):
+        code = op.opcode
+        rt = op.result_type
+        shape = tuple(rt.shape)
+        kind = _kind_of(rt)
+        at = op.attrs
+        if code == "constant":
+            return self.const(np.asarray(at["value"]).reshape(shape), kind)
+        if code == "iota":
+            d = at["dim"]
+            mid = [1] * len(shape)
+            mid[d] = shape[d]
+            ramp = np.arange(shape[d], dtype=_NP_DTYPE[kind]).reshape(mid)
+            return self.const(np.broadcast_to(ramp, shape), kind)
+        if code == "transpose":
+            (a,) = ins
+            p = at["perm"]
+            return Val(a.buf, a.off, tuple(a.shape[i] for i in p),
+                       tuple(a.st[i] for i in p), a.kind, a.alloc)
+        if code == "slice":
+            (a,) = ins
+            off = a.off + sum(s * t for s, t in zip(at["start"], a.st))
+            return Val(a.buf, off, shape, a.st, a.kind, a.alloc)
+        if code == "reshape":
+            return self.reshape(ins[0], shape, idx)
+        if code == "broadcast_in_dim":
+            (a,) = ins
+            mid = [1] * len(shape)
+            for s, d in enumerate(at["dims"]):
+                mid[d] = a.shape[s]
+            m = self.reshape(a, tuple(mid), idx)
+            st = tuple(0 if (mid[d] == 1 and shape[d] != 1) else m.st[d]
+                       for d in range(len(shape)))
+            return Val(m.buf, m.off, shape, st, m.kind, m.alloc)
+        if code in B_CODES:
+            st = L.keep_order_strides(shape, [ins[0].st, ins[1].st])
+            out = self.result_val(op, shape, st, kind)
+            self.emit(OP_BINARY, B_CODES[code], out, ins)
+            return out
+        if code == "compare":
+            st = L.keep_order_strides(shape, [ins[0].st, ins[1].st])
+            out = self.result_val(op, shape, st, kind)
+            self.emit(OP_BINARY, CMP_CODES[at["kind"]], out, ins)
+            return out
+        if code in ("negate", "exponential", "log"):
+            st = L.keep_order_strides(shape, [ins[0].st])
+            out = self.result_val(op, shape, st, kind)
+            sub = {"negate": U_NEG, "exponential": U_EXP, "log": U_LOG}[code]
+            self.emit(OP_UNARY, sub, out, ins)
+            return out
+        if code == "convert":
+            st = L.keep_order_strides(shape, [ins[0].st])
+            out = self.result_val(op, shape, st, kind)
+            self.emit(OP_UNARY, U_CVT, out, ins)
+            return out
+        if code == "select":
+            st = L.keep_order_strides(shape, [v.st for v in ins])
+            out = self.result_val(op, shape, st, kind)
+            self.emit(OP_SELECT, 0, out, ins, kin=ins[1].kind)
+            return out
+        if code == "dot":
+            a, b = ins
+            out = self.result_val(op, shape, L.c_strides(shape), kind)
+            m1, split, m2 = dot_modes(a, b)
+            self.emit(OP_DOT, m1, out, ins, aux=[a.shape[1], split, m2])
+            return out
+        if code == "reduce":
+            (a,) = ins
+            ax = at["axis"]
+            perm = L.best_axis_order(len(a.shape), [a.st])
+            rest = [p for p in perm if p != ax]
+            keep = [d for d in range(len(a.shape)) if d != ax]
+            # allocate the result following the input's axis order (order K)
+            sub_perm = [keep.index(p) for p in rest]
+            st = L.strides_for_order(shape, sub_perm) if shape else ()
+            out = self.result_val(op, shape, st, kind)
+            if at["kind"] == "max":
+                sub = R_MAX
+            elif perm[0] == ax and a.shape[ax] > 1:
+                sub = R_SUM_PAIRWISE
+            else:
+                sub = R_SUM_SEQ
+            src = Val(a.buf, a.off, tuple(a.shape[d] for d in keep),
+                      tuple(a.st[d] for d in keep), a.kind, a.alloc)
+            self.emit(OP_REDUCE, sub, out, [src], aux=[a.shape[ax], a.st[ax]])
+            return out
+        if code == "pad":
+            a, pv = ins
+            fnc = L.is_f_contiguous(a.shape, a.st) and not \
+                L.is_c_contiguous(a.shape, a.st)
+            st = L.strides_for_order(shape, list(range(len(shape)))) if fnc \
+                else L.c_strides(shape)
+            out = self.result_val(op, shape, st, kind)
+            self.emit(OP_PAD, 0, out, [a, pv], aux=list(at["low"]),
+                      aux2=list(a.shape))
+            return out
+        raise LoweringError(f"cannot lower opcode {code!r}")
+
+    def reshape(self, a: Val, shape, idx):
+        st = L.reshape_view(a.shape, a.st, shape)
+        if st is not None:
+            return Val(a.buf, a.off, tuple(shape), st, a.kind, a.alloc)
+        # numpy copies into C order, then reinterprets
+        tmp = self.fresh(a.shape, L.c_strides(a.shape), a.kind,
+                         int(np.prod(a.shape, dtype=np.int64)))
+        self.emit(OP_UNARY, U_COPY, tmp, [a])
+        return Val(tmp.buf, tmp.off, tuple(shape), L.c_strides(shape),
+                   tmp.kind, tmp.alloc)
+
+    # -- arena assignment ---------------------------------------------------------
+    def assign_arena(self):
+        """First-fit by liveness over the instruction list: an allocation
+        lives from the instruction that writes it to the last instruction
+        reading it, so an instruction never writes over its own operands."""
+        created, last_read = {}, {}
+        for i, ins in enumerate(self.instrs):
+            a = ins["out"].alloc
+            if a >= 0 and self.allocs[a].fixed is None:
+                created.setdefault(a, i)
+            for v in ins["in"]:
+                if v.alloc >= 0:
+                    last_read[v.alloc] = i
+        live, top = [], 0
+        for a_id, i in sorted(created.items(), key=lambda kv: kv[1]):
+            a = self.allocs[a_id]
+            live = sorted(x for x in live if x[2] >= i)
+            pos = 0
+            for off, size, _ in live:
+                if pos + a.size <= off:
+                    break
+                pos = max(pos, off + size)
+            a.off = pos
+            live.append((pos, a.size, max(i, last_read.get(a_id, i))))
+            top = max(top, pos + a.size)
+        return top
+
+
+def _op_cost(op, tys, table):
+    unit = table.get(op.opcode, 1.0)
+    if op.opcode == "dot":
+        a, b = tys
+        return unit * a.shape[0] * b.shape[1] * a.shape[1]
+    if op.opcode == "reduce":
+        return unit * _count(tys[0].shape)
+    return unit * _count(op.result_type.shape)
+
+
+def _count(shape):
+    n = 1
+    for d in shape:
+        n *= d
+    return n
+
+
+def static_cost(fn, cost_table=None) -> float:
+    """ExecPlan.total_cost (interpreter.py:205-214): float sum in op order."""
+    types = dict(fn.params)
+    total = 0.0
+    for op in fn.ops:
+        total += _op_cost(op, tuple(types[v] for v in op.operands),
+                          cost_table or {})
+        types[op.result] = op.result_type
+    return total
+
+
+def lower_function(fn, param_layouts=None, ret_bufs=None, ret_layout="compact",
+                   cost_table=None) -> Lowered:
+    """Lower one function.  Params i live in buffer PARAM0+i with the given
+    element strides (default: C order); return r is written to ret_bufs[r]
+    (default: (OUT0+r, 0))."""
+    params = []
+    for i, (name, ty) in enumerate(fn.params):
+        shape = tuple(ty.shape)
+        st = tuple(param_layouts[i]) if param_layouts else L.c_strides(shape)
+        params.append(Val(BUF_PARAM0 + i, 0, shape, st, _kind_of(ty)))
+    if ret_bufs is None:
+        ret_bufs = [(BUF_OUT0 + r, 0) for r in range(len(fn.returns))]
+    b = _Builder(fn, params, ret_bufs, ret_layout, cost_table)
+    ret_st = b.run(fn.returns)
+    top = b.assign_arena()
+    # resolve arena offsets into the operands
+    instrs = []
+    for rec in b.instrs:
+        fixed = []
+        for v in [rec["out"]] + rec["in"]:
+            if v.alloc >= 0 and v.buf == BUF_ARENA:
+                a = b.allocs[v.alloc]
+                fixed.append(Val(BUF_ARENA, a.off + v.off, v.shape, v.st, v.kind))
+            else:
+                fixed.append(v)
+        rec = dict(rec)
+        rec["out"], rec["in"] = fixed[0], fixed[1:]
+        instrs.append(rec)
+    return Lowered(instrs, b.consts, top, ret_st, b.cost)
+
+
+AM_STRIDED, AM_LINEAR, AM_SCALAR = 0, 1, 2
+
+
+def _addr_mode(v, shape):
+    """How the executor addresses an elementwise operand (exec_core.cuh)."""
+    if all(s == 0 or d == 1 for s, d in zip(v.st, shape)):
+        return AM_SCALAR
+    cst = L.c_strides(shape)
+    if all(s == c or d == 1 for s, c, d in zip(v.st, cst, shape)):
+        return AM_LINEAR
+    return AM_STRIDED
+
+
+def encode_instrs(instrs, const_base=0) -> np.ndarray:
+    arr = np.zeros(len(instrs), dtype=INSTR_DTYPE)
+    for i, rec in enumerate(instrs):
+        e = arr[i]
+        for k in ("op", "sub", "kout", "kin", "rank", "n"):
+            e[k] = rec[k]
+        e["shp"] = rec["shp"]
+        e["aux"] = rec["aux"]
+        e["aux2"] = rec["aux2"]
+        if rec["op"] in (OP_UNARY, OP_BINARY, OP_SELECT):
+            shape = tuple(rec["out"].shape)
+            modes = [_addr_mode(rec["out"], shape)]
+            modes += [_addr_mode(v, shape) for v in rec["in"]]
+            modes += [AM_SCALAR] * (4 - len(modes))
+            e["aux2"] = modes + [0] * (MAXR - 4)
+        for slot, v in [("out", rec["out"])]:
+            e[slot]["buf"] = v.buf
+            e[slot]["off"] = v.off
+            e[slot]["st"] = list(v.st) + [0] * (MAXR - len(v.st))
+        for j, v in enumerate(rec["in"]):
+            e["in"][j]["buf"] = v.buf
+            e["in"][j]["off"] = v.off
+            e["in"][j]["st"] = list(v.st) + [0] * (MAXR - len(v.st))
+    return arr
+
+
+def consts_to_words(consts) -> np.ndarray:
+    """Constant pool as 64-bit words (float64 bits or int64)."""
+    out = np.zeros(len(consts), dtype=np.float64)
+    iv = out.view(np.int64)
+    for i, c in enumerate(consts):
+        if isinstance(c, float):
+            out[i] = c
+        else:
+            iv[i] = int(c)
+    return out

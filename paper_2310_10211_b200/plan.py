@@ -1,0 +1,235 @@
+"""Population plan: many lowered variants packed into one launch blob.
+
+One `PopulationPlan` per evaluator call (a generation's fresh individuals):
+the per-individual `ExecPlan` objects of the reference (interpreter.py:
+188-239, cached per FunctionBody) become rows of a single instruction table
+that the device executor walks, one CTA per individual.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import layout as L
+from .lowering import (BUF_OUT0, FLAG_LAYOUT_APPROX, HEADER_DTYPE,
+                       INSTR_DTYPE, PLAN_MAGIC, PLAN_VERSION, PROG_DTYPE,
+                       consts_to_words, encode_instrs, lower_function,
+                       static_cost)
+
+
+@dataclass
+class VariantPlan:
+    """Lowered functions of one individual."""
+    train0: list | None
+    train1: list | None
+    fwd: list
+    consts: list
+    arena: int
+    flags: int
+    train_cost: float
+    fwd_cost: float
+
+
+def _count(shape):
+    n = 1
+    for d in shape:
+        n *= d
+    return n
+
+
+def lower_variant(functions: dict, cost_table=None, training=True,
+                  weight_layouts=None) -> VariantPlan:
+    """functions: {'train_step': fn, 'forward': fn} (train_step only in
+    training mode).  Weight params start C-ordered like the module
+    constants; steps >= 1 see the layout the previous step stored."""
+    consts: list = []
+    arena = 0
+    flags = 0
+    t0 = t1 = None
+    train_cost = 0.0
+    fwd_layouts = weight_layouts
+    if training:
+        ts = functions["train_step"]
+        nw = len(ts.returns)
+        c_layout = [L.c_strides(tuple(t.shape)) for _, t in ts.params]
+        low0 = lower_function(ts, c_layout, cost_table=cost_table)
+        train_cost = low0.cost
+        layouts = list(c_layout)
+        layouts[:nw] = low0.ret_strides
+        if tuple(low0.ret_strides) == tuple(c_layout[:nw]):
+            low1 = low0
+        else:
+            low1 = lower_function(ts, layouts, cost_table=cost_table)
+            if tuple(low1.ret_strides) != tuple(low0.ret_strides):
+                # a second change: take the layout after step 1 for all
+                # later steps and flag it (never seen on the MLP workloads)
+                layouts[:nw] = low1.ret_strides
+                low1 = lower_function(ts, layouts, cost_table=cost_table)
+                flags |= FLAG_LAYOUT_APPROX
+        t0 = _shift_consts(low0, consts)
+        t1 = t0 if low1 is low0 else _shift_consts(low1, consts)
+        arena = max(low0.arena_elems, low1.arena_elems)
+        fwd_layouts = list(low1.ret_strides)
+    fw = functions["forward"]
+    nwf = len(fw.params) - 1
+    f_layout = [L.c_strides(tuple(t.shape)) for _, t in fw.params]
+    if fwd_layouts is not None:
+        f_layout[:nwf] = fwd_layouts[:nwf]
+    lowf = lower_function(fw, f_layout, ret_layout="c", cost_table=cost_table)
+    f = _shift_consts(lowf, consts)
+    arena = max(arena, lowf.arena_elems)
+    return VariantPlan(t0, t1, f, consts, arena, flags, train_cost, lowf.cost)
+
+
+def _shift_consts(low, pool):
+    """Append a function's constants to the individual's pool and rebase
+    its CONST operands."""
+    base = len(pool)
+    pool.extend(low.consts)
+    if base == 0:
+        return low.instrs
+    out = []
+    for rec in low.instrs:
+        rec = dict(rec)
+        rec["in"] = [_rebase(v, base) for v in rec["in"]]
+        out.append(rec)
+    return out
+
+
+def _rebase(v, base):
+    if v.buf == 1:  # BUF_CONST
+        from .lowering import Val
+        return Val(v.buf, v.off + base, v.shape, v.st, v.kind, v.alloc)
+    return v
+
+
+@dataclass
+class PopulationPlan:
+    blob: np.ndarray          # uint8 bytes handed to gevo_eval
+    n_prog: int
+    order: np.ndarray         # launch order (individual index per CTA)
+    total_elems: int
+
+
+def build_population_plan(variants: list[VariantPlan], weight_shapes,
+                          probs_elems: int, order=None) -> PopulationPlan:
+    """Pack variants into one blob.  `order` is the launch order (CTA i runs
+    individual order[i]); by default longest static cost first, so the
+    slowest individuals start in the first wave."""
+    n = len(variants)
+    if order is None:
+        key = np.array([v.train_cost * 1.0 + v.fwd_cost for v in variants])
+        order = np.argsort(-key, kind="stable")
+    wsizes = [_count(s) for s in weight_shapes]
+    wofs = np.concatenate([[0], np.cumsum(wsizes)]).astype(np.int64)
+    wtotal = int(wofs[-1])
+    instr_chunks, const_chunks = [], []
+    progs = np.zeros(n, dtype=PROG_DTYPE)
+    n_instr = n_const = 0
+    elem = 0
+    max_arena = 0
+    for slot, idx in enumerate(order):
+        v = variants[idx]
+        p = progs[slot]
+        p["result_slot"] = idx
+        p["const_off"] = n_const
+        const_chunks.append(consts_to_words(v.consts))
+        n_const += len(v.consts)
+        if v.train0 is not None:
+            a = encode_instrs(v.train0)
+            p["train0"], p["train0_n"] = n_instr, len(a)
+            instr_chunks.append(a)
+            n_instr += len(a)
+            if v.train1 is v.train0:
+                p["train1"], p["train1_n"] = p["train0"], p["train0_n"]
+            else:
+                b = encode_instrs(v.train1)
+                p["train1"], p["train1_n"] = n_instr, len(b)
+                instr_chunks.append(b)
+                n_instr += len(b)
+        f = encode_instrs(v.fwd)
+        p["fwd"], p["fwd_n"] = n_instr, len(f)
+        instr_chunks.append(f)
+        n_instr += len(f)
+        arena = (v.arena + 15) & ~15
+        p["arena_off"] = elem
+        p["arena_elems"] = arena
+        p["flags"] = v.flags
+        max_arena = max(max_arena, arena)
+        # [scratch | probs | weights ping | weights pong], 16-element aligned
+        elem += arena + ((probs_elems + 15) & ~15) + 2 * ((wtotal + 15) & ~15)
+    hdr = np.zeros(1, dtype=HEADER_DTYPE)
+    hdr["magic"], hdr["version"] = PLAN_MAGIC, PLAN_VERSION
+    hdr["n_instr"], hdr["n_prog"], hdr["n_const"] = n_instr, n, n_const
+    hdr["weight_elems"] = wtotal
+    hdr["n_weights"] = len(wsizes)
+    hdr["wofs"][0, :len(wsizes)] = wofs[:-1]
+    hdr["max_arena"] = max_arena
+    hdr["total_elems"] = elem
+    instrs = np.concatenate(instr_chunks) if instr_chunks else \
+        np.zeros(0, dtype=INSTR_DTYPE)
+    consts = np.concatenate(const_chunks) if const_chunks else np.zeros(0)
+    blob = np.concatenate([hdr.view(np.uint8), instrs.view(np.uint8),
+                           progs.view(np.uint8), consts.view(np.uint8)])
+    return PopulationPlan(blob, n, np.asarray(order), elem)
+
+
+def exec_once_plan(fns, param_arrays_list):
+    """Plan for running one function once per case with explicit params
+    (per-op and single-step parity tests).  Returns (blob, params_blob,
+    out_sizes, out_offsets_per_case, out_total)."""
+    n = len(fns)
+    progs = np.zeros(n, dtype=PROG_DTYPE)
+    chunks, consts_c = [], []
+    params_flat = []
+    n_instr = n_const = 0
+    pofs = 0
+    oofs = 0
+    elem = 0
+    out_meta = []
+    for i, (fn, params) in enumerate(zip(fns, param_arrays_list)):
+        low = lower_function(fn, None, ret_layout="c")
+        a = encode_instrs(low.instrs)
+        p = progs[i]
+        p["train0"], p["train0_n"] = n_instr, len(a)
+        p["const_off"] = n_const
+        p["result_slot"] = i
+        chunks.append(a)
+        n_instr += len(a)
+        consts_c.append(consts_to_words(low.consts))
+        n_const += len(low.consts)
+        for k, arr in enumerate(params):
+            words = np.ascontiguousarray(arr)
+            if words.dtype == np.bool_:
+                words = words.astype(np.int64)
+            words = words.reshape(-1).view(np.float64) if words.dtype != np.float64 \
+                else words.reshape(-1)
+            p["param_off"][k] = pofs
+            params_flat.append(words)
+            pofs += len(words)
+        metas = []
+        for r, ty in enumerate(fn.return_types):
+            cnt = _count(tuple(ty.shape))
+            p["out_off"][r] = oofs
+            metas.append((oofs, tuple(ty.shape), getattr(ty.kind, "value", ty.kind)))
+            oofs += max(cnt, 1)
+        out_meta.append(metas)
+        arena = (low.arena_elems + 15) & ~15
+        p["arena_off"] = elem
+        p["arena_elems"] = arena
+        elem += arena + 16
+    hdr = np.zeros(1, dtype=HEADER_DTYPE)
+    hdr["magic"], hdr["version"] = PLAN_MAGIC, PLAN_VERSION
+    hdr["n_instr"], hdr["n_prog"], hdr["n_const"] = n_instr, n, n_const
+    hdr["total_elems"] = elem
+    instrs = np.concatenate(chunks) if chunks else np.zeros(0, dtype=INSTR_DTYPE)
+    consts = np.concatenate(consts_c) if consts_c else np.zeros(0)
+    blob = np.concatenate([hdr.view(np.uint8), instrs.view(np.uint8),
+                           progs.view(np.uint8), consts.view(np.uint8)])
+    params_blob = np.concatenate(params_flat) if params_flat else np.zeros(1)
+    return blob, params_blob, out_meta, max(oofs, 1)
+
+
+__all__ = ["lower_variant", "build_population_plan", "exec_once_plan",
+           "static_cost", "VariantPlan", "PopulationPlan"]

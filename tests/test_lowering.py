@@ -1,0 +1,184 @@
+"""Host lowering: cost identity, layout model, and the instruction tables
+walked on CPU by tests/tools/plan_emu.py (no GPU needed)."""
+import numpy as np
+import pytest
+
+from golden_io import dec, load, variant_functions
+from oracle import interp as OI
+from paper_2310_10211_b200 import dialect, layout as L, lowering as Lw
+from paper_2310_10211_b200 import workloads as W
+from paper_2310_10211_b200.plan import (build_population_plan, exec_once_plan,
+                                        lower_variant)
+from tools import plan_emu
+
+
+def _words(a):
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.bool_:
+        a = a.astype(np.int64)
+    if a.dtype == np.float64:
+        return a.reshape(-1).view(np.int64).copy()
+    return a.reshape(-1).astype(np.int64)
+
+
+def emulate(fn, params, param_layouts=None):
+    low = Lw.lower_function(fn, param_layouts, ret_layout="c")
+    consts = Lw.consts_to_words(low.consts).view(np.int64).copy() if low.consts \
+        else np.zeros(1, dtype=np.int64)
+    mem = {Lw.BUF_ARENA: np.zeros(max(low.arena_elems, 1), dtype=np.int64),
+           Lw.BUF_CONST: consts}
+    for k, p in enumerate(params):
+        mem[Lw.BUF_PARAM0 + k] = _words(p)
+    for r, ty in enumerate(fn.return_types):
+        mem[Lw.BUF_OUT0 + r] = np.zeros(max(1, int(np.prod(ty.shape))), dtype=np.int64)
+    plan_emu.run(low.instrs, mem)
+    outs = []
+    for r, ty in enumerate(fn.return_types):
+        w = mem[Lw.BUF_OUT0 + r][:max(1, int(np.prod(ty.shape)))]
+        k = dialect.kind_name(ty.kind)
+        arr = w.view(np.float64) if k == "f32" else (w != 0 if k == "i1" else w)
+        outs.append(arr.reshape(ty.shape))
+    return outs, low
+
+
+def test_static_cost_is_reference_cost():
+    pop = load("train_pop.json.gz")["individuals"]
+    for ind in pop:
+        fns = variant_functions(ind)
+        assert Lw.static_cost(fns["train_step"]) * 600 == ind["cost"]
+        vp = lower_variant(fns)
+        assert vp.train_cost * 600 == ind["cost"]
+    for ind in load("predict_pop.json.gz")["individuals"]:
+        fns = variant_functions(ind, ("forward",))
+        assert Lw.static_cost(fns["forward"]) * 31 == ind["cost"]
+
+
+def test_every_opcase_lowers_and_emulates():
+    for c in load("opcases.json.gz")["cases"]:
+        fn = dialect.parse_function(c["text"])
+        params = [dec(o).reshape(t.shape) for o, (_, t) in zip(c["operands"], fn.params)]
+        (got,), _ = emulate(fn, params)
+        exp = dec(c["expected"])
+        got = np.asarray(got).reshape(exp.shape)
+        if exp.dtype == np.float64:
+            assert np.allclose(got, exp, rtol=1e-12, atol=1e-12, equal_nan=True), c["text"]
+        else:
+            assert np.array_equal(got.astype(exp.dtype), exp), c["text"]
+
+
+def test_train_step_tables_emulate_one_step():
+    wl = W.build_2fcnet_workload()
+    w0 = [wl.weights[n] for n in W.WEIGHT_NAMES]
+    args = w0 + [wl.search_x[0], wl.search_y[0]]
+    for ind in load("train_pop.json.gz")["individuals"]:
+        fn = dialect.parse_function(ind["train_step"])
+        ref = OI.Program(fn)(args)
+        got, _ = emulate(fn, args)
+        for a, b in zip(got, ref):
+            assert np.allclose(a, np.asarray(b), rtol=1e-11, atol=1e-13, equal_nan=True)
+
+
+def test_population_plan_packs():
+    pop = load("train_pop.json.gz")["individuals"][:20]
+    vps = [lower_variant(variant_functions(i)) for i in pop]
+    plan = build_population_plan(vps, [(784, 32), (32,), (32, 10), (10,)], 320)
+    hdr = plan.blob[:Lw.HEADER_DTYPE.itemsize].view(Lw.HEADER_DTYPE)[0]
+    assert hdr["magic"] == Lw.PLAN_MAGIC and hdr["n_prog"] == 20
+    assert hdr["weight_elems"] == 784 * 32 + 32 + 320 + 10
+    n_instr = hdr["n_instr"]
+    expect = (Lw.HEADER_DTYPE.itemsize + n_instr * Lw.INSTR_DTYPE.itemsize +
+              20 * Lw.PROG_DTYPE.itemsize + hdr["n_const"] * 8)
+    assert plan.blob.nbytes == expect
+    # longest static cost first
+    costs = [vps[i].train_cost + vps[i].fwd_cost for i in plan.order]
+    assert costs == sorted(costs, reverse=True)
+
+
+def test_exec_once_plan_layout():
+    c = load("opcases.json.gz")["cases"][0]
+    fn = dialect.parse_function(c["text"])
+    params = [dec(o) for o in c["operands"]]
+    blob, pblob, meta, total = exec_once_plan([fn], [params])
+    assert blob.dtype == np.uint8 and total >= 1
+
+
+# --- the numpy layout model ----------------------------------------------------
+
+def _np_strides(a):
+    return tuple(s // a.itemsize for s in a.strides)
+
+
+@pytest.mark.parametrize("shape", [(4, 5), (3, 4, 5), (2, 3, 4, 2)])
+def test_keep_order_matches_numpy_ufunc_allocation(shape):
+    rng = np.random.default_rng(0)
+    base = np.zeros(shape)
+    for _ in range(30):
+        perm = tuple(rng.permutation(len(shape)))
+        a = np.transpose(np.zeros(tuple(shape[p] for p in np.argsort(perm))), perm) \
+            if rng.random() < 0.5 else base
+        b = np.transpose(np.zeros(tuple(shape[p] for p in np.argsort(perm))), perm) \
+            if rng.random() < 0.5 else base
+        a = np.ascontiguousarray(a) if a.shape != shape else a
+        if a.shape != shape or b.shape != shape:
+            continue
+        got = L.keep_order_strides(shape, [_np_strides(a), _np_strides(b)])
+        assert got == _np_strides(a + b)
+        assert L.keep_order_strides(shape, [_np_strides(a)]) == _np_strides(np.exp(a))
+
+
+def test_reshape_view_matches_numpy():
+    rng = np.random.default_rng(1)
+    for _ in range(300):
+        shape = tuple(int(x) for x in rng.integers(1, 4, size=rng.integers(1, 4)))
+        a = np.zeros(shape)
+        if rng.random() < 0.5 and a.ndim > 1:
+            a = a.transpose(tuple(rng.permutation(a.ndim)))
+        n = a.size
+        # random factorisation of n
+        dims, m = [], n
+        while m > 1 and len(dims) < 3:
+            f = [d for d in range(1, m + 1) if m % d == 0]
+            d = int(rng.choice(f))
+            dims.append(d)
+            m //= d
+        dims.append(m)
+        new = tuple(dims)
+        r = np.reshape(a, new)
+        got = L.reshape_view(a.shape, _np_strides(a), new)
+        if np.shares_memory(r, a):
+            assert got is not None
+            # strides may differ only on extent-1 dims
+            assert all(g == s or d == 1 for g, s, d in zip(got, _np_strides(r), new))
+        else:
+            assert got is None
+
+
+def _running_sum(row):
+    r = 0.0          # not sum(): CPython 3.12 sums floats with compensation
+    for x in row.tolist():
+        r += x
+    return r
+
+
+def test_reduce_order_matches_numpy():
+    """Pairwise vs running sum is decided like numpy: probe with values
+    whose two summation orders round differently."""
+    rng = np.random.default_rng(2)
+    for _ in range(200):
+        shape = tuple(int(x) for x in rng.integers(2, 20, size=2))
+        a = rng.standard_normal(shape) * 10.0 ** rng.integers(-8, 8, size=shape)
+        if rng.random() < 0.5:
+            a = np.ascontiguousarray(a.T).T
+        ax = int(rng.integers(0, 2))
+        perm = L.best_axis_order(2, [_np_strides(a)])
+        pairwise = perm[0] == ax and a.shape[ax] > 1
+        moved = np.moveaxis(a, ax, -1).reshape(-1, a.shape[ax])
+        ref = np.sum(a, axis=ax).reshape(-1)
+        seq = np.array([_running_sum(row) for row in moved])
+        if pairwise:
+            # numpy pairwise for n < 8 is the running sum anyway
+            from tools_sum import pairwise_sum
+            want = np.array([pairwise_sum(row) for row in moved])
+        else:
+            want = seq
+        assert np.array_equal(want, ref)

@@ -1,0 +1,114 @@
+"""Vectorised CPU walker of a lowered instruction table (TEST TOOL ONLY).
+
+It checks the *lowering* (addressing, view folding, layouts, arena reuse,
+return placement) independently of the GPU: it executes the records that
+lowering.lower_function produces with plain numpy arithmetic (no attempt at
+numpy's summation order), so results agree with the oracle to ~1e-12, not
+bit-exactly.  Never used by the product or the bench.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2310_10211_b200 import lowering as Lw
+
+F = Lw.K_F64
+
+
+def offsets(v, shape):
+    if not shape:
+        return np.array([v.off], dtype=np.int64)
+    grids = np.indices(shape, dtype=np.int64).reshape(len(shape), -1)
+    st = np.array(v.st[:len(shape)], dtype=np.int64)
+    return v.off + (grids * st[:, None]).sum(0)
+
+
+def gather(mem, v, shape):
+    return mem[v.buf][offsets(v, shape)]
+
+
+def scatter(mem, v, shape, words):
+    mem[v.buf][offsets(v, shape)] = words
+
+
+def fl(w):
+    return np.asarray(w, dtype=np.int64).view(np.float64)
+
+
+def wd(x):
+    return np.asarray(x, dtype=np.float64).view(np.int64)
+
+
+def run(instrs, mem):
+    """mem: dict buf_id -> np.ndarray of int64 words (float64 bits)."""
+    for rec in instrs:
+        op, sub = rec["op"], rec["sub"]
+        out = rec["out"]
+        shape = tuple(out.shape)
+        kin, kout = rec["kin"], rec["kout"]
+        with np.errstate(all="ignore"):
+            if op == Lw.OP_SELECT:
+                p, t, f = (gather(mem, v, shape) for v in rec["in"])
+                r = np.where(p != 0, t, f)
+            elif op == Lw.OP_UNARY:
+                a = gather(mem, rec["in"][0], shape)
+                if sub == Lw.U_COPY:
+                    r = a
+                elif sub == Lw.U_CVT:
+                    if kout == Lw.K_I1:
+                        r = ((fl(a) != 0) if kin == F else (a != 0)).astype(np.int64)
+                    elif kout == Lw.K_I64:
+                        r = np.trunc(fl(a)).astype(np.int64) if kin == F else a
+                    else:
+                        r = a if kin == F else wd(a.astype(np.float64))
+                elif kin == F:
+                    x = fl(a)
+                    r = wd({Lw.U_NEG: -x, Lw.U_EXP: np.exp(x), Lw.U_LOG: np.log(x)}[sub])
+                else:
+                    r = -a
+            elif op == Lw.OP_BINARY:
+                a = gather(mem, rec["in"][0], shape)
+                b = gather(mem, rec["in"][1], shape)
+                if kin == F:
+                    x, y = fl(a), fl(b)
+                    if sub <= 4:
+                        r = wd([x + y, x - y, x * y, np.true_divide(x, y),
+                                np.maximum(x, y)][sub])
+                    else:
+                        r = [x == y, x != y, x < y, x <= y, x > y, x >= y][sub - 5].astype(np.int64)
+                else:
+                    if sub == 3:
+                        nz = b != 0
+                        q = np.trunc(np.true_divide(a, np.where(nz, b, 1)))
+                        r = np.where(nz, q, 0).astype(np.int64)
+                    elif sub <= 4:
+                        r = [a + b, a - b, a * b, None, np.maximum(a, b)][sub]
+                    else:
+                        r = [a == b, a != b, a < b, a <= b, a > b, a >= b][sub - 5].astype(np.int64)
+            elif op == Lw.OP_REDUCE:
+                L, rs = rec["aux"][0], rec["aux"][1]
+                base = offsets(rec["in"][0], shape)
+                idx = base[:, None] + np.arange(L, dtype=np.int64)[None, :] * rs
+                w = mem[rec["in"][0].buf][idx]
+                if kin == F:
+                    x = fl(w)
+                    r = wd(np.max(x, axis=1) if sub == Lw.R_MAX else np.sum(x, axis=1))
+                else:
+                    r = np.max(w, axis=1) if sub == Lw.R_MAX else np.sum(w, axis=1)
+            elif op == Lw.OP_DOT:
+                a, b = rec["in"]
+                M, N, K = shape[0], shape[1], rec["aux"][0]
+                A = gather(mem, a, (M, K)).reshape(M, K)
+                B = gather(mem, b, (K, N)).reshape(K, N)
+                r = wd(fl(A) @ fl(B)) if kin == F else A @ B
+            elif op == Lw.OP_PAD:
+                a, pv = rec["in"]
+                low, ext = rec["aux"][:len(shape)], rec["aux2"][:len(shape)]
+                src = gather(mem, a, tuple(ext)).reshape(ext)
+                pval = mem[pv.buf][pv.off]
+                full = np.full(shape, pval, dtype=np.int64)
+                full[tuple(slice(l, l + e) for l, e in zip(low, ext))] = src
+                r = full
+            else:
+                raise ValueError(f"unknown op {op}")
+        scatter(mem, out, shape, np.asarray(r, dtype=np.int64).reshape(-1))
