@@ -143,16 +143,93 @@ __device__ __forceinline__ double dot_elem(int mode, const double* a, int64_t sa
   return r;
 }
 
+// D(8x8) += A(8x4) B(4x8) on the FP64 tensor path.  Probed on B200:
+// bit-identical to four chained fma() in k order (tests/tools/dmma_probe.cu),
+// so an 8x8 tile accumulated over k0 = 0, 4, 8, ... reproduces the
+// reference's single-accumulator FMA chain (OpenBLAS dgemm kernels) exactly.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// FMA-chain dot over output columns [0, ncols): one warp owns an 8x16 strip
+// (two 8x8 tiles sharing the A fragment) for the whole K range -- never a
+// split-K, which would change the summation order.
+__device__ void dot_fma_dmma(const gevo_instr& I, double* out, const double* A,
+                             const double* B, int ncols) {
+  const int M = I.shp[0], K = I.aux[0];
+  const int64_t sam = I.in[0].st[0], sak = I.in[0].st[1];
+  const int64_t sbk = I.in[1].st[0], sbn = I.in[1].st[1];
+  const int64_t som = I.out.st[0], son = I.out.st[1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int tm = (M + 7) >> 3, tn2 = (ncols + 15) >> 4;
+  const int K4 = K & ~3;
+  A += I.in[0].off;
+  B += I.in[1].off;
+  for (int tile = warp; tile < tm * tn2; tile += nwarp) {
+    const int ti = tile / tn2, tj = tile - ti * tn2;
+    const int i = ti * 8 + g;                 // A-fragment row of this lane
+    const int j0 = tj * 16 + g, j1 = j0 + 8;  // B-fragment columns of this lane
+    const bool vi = i < M, v0 = j0 < ncols, v1 = j1 < ncols;
+    const double* pa = A + (vi ? i : 0) * sam + t4 * sak;
+    const double* pb0 = B + (v0 ? j0 : 0) * sbn + t4 * sbk;
+    const double* pb1 = B + (v1 ? j1 : 0) * sbn + t4 * sbk;
+    const int64_t ska = 4 * sak, skb = 4 * sbk;
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+#pragma unroll 4
+    for (int k0 = 0; k0 < K4; k0 += 4) {
+      const double a = vi ? *pa : 0.0;
+      const double b0 = v0 ? *pb0 : 0.0;
+      const double b1 = v1 ? *pb1 : 0.0;
+      dmma884(c00, c01, a, b0);
+      dmma884(c10, c11, a, b1);
+      pa += ska;
+      pb0 += skb;
+      pb1 += skb;
+    }
+    // D fragment: row ti*8+g, columns tj*16 + {2t4, 2t4+1} and +8
+    const int r = ti * 8 + g;
+    const int cA = tj * 16 + 2 * t4, cB = cA + 8;
+    if (K4 < K && r < M) {                    // k tail, same chain order
+      const double* ar = A + r * sam;
+      for (int k = K4; k < K; ++k) {
+        const double a = ar[k * sak];
+        const double* bk = B + k * sbk;
+        if (cA < ncols) c00 = fma(a, bk[cA * sbn], c00);
+        if (cA + 1 < ncols) c01 = fma(a, bk[(cA + 1) * sbn], c01);
+        if (cB < ncols) c10 = fma(a, bk[cB * sbn], c10);
+        if (cB + 1 < ncols) c11 = fma(a, bk[(cB + 1) * sbn], c11);
+      }
+    }
+    if (r < M) {
+      double* o = out + I.out.off + r * som;
+      if (cA < ncols) o[cA * son] = c00;
+      if (cA + 1 < ncols) o[(cA + 1) * son] = c01;
+      if (cB < ncols) o[cB * son] = c10;
+      if (cB + 1 < ncols) o[(cB + 1) * son] = c11;
+    }
+  }
+}
+
 __device__ void run_dot(const Shared& S, const gevo_instr& I) {
   double* out = opptr(S, I.out);
   const double* A = opptr(S, I.in[0]);
   const double* B = opptr(S, I.in[1]);
-  const int M = I.shp[0], N = I.shp[1], K = I.aux[0], split = I.aux[1];
+  const int M = I.shp[0], N = I.shp[1], K = I.aux[0];
+  int split = I.aux[1];
   const int64_t sam = I.in[0].st[0], sak = I.in[0].st[1];
   const int64_t sbk = I.in[1].st[0], sbn = I.in[1].st[1];
   const bool f = I.kin == GEVO_K_F64;
-  for (int e = threadIdx.x; e < M * N; e += blockDim.x) {
-    int i = e / N, j = e - i * N;
+  int first = 0;  // columns [0, first) done on the tensor path
+  if (f && I.sub == GEVO_D_FMA_CHAIN && split > 0) {
+    dot_fma_dmma(I, out, A, B, split);
+    first = split;
+    if (first >= N) return;
+  }
+  const int span = N - first;
+  for (int e = threadIdx.x; e < M * span; e += blockDim.x) {
+    int i = e / span, j = first + (e - i * span);
     const double* a = A + I.in[0].off + i * sam;
     const double* b = B + I.in[1].off + j * sbn;
     double r;

@@ -187,3 +187,21 @@ def test_nsga2_bit_exact(ctx):
         for n, chosen in s["survivors"].items():
             got, _, _ = ctx.nsga2_select(pts[:, 0], pts[:, 1], int(n))
             assert got.tolist() == chosen
+
+
+def test_device_exp_is_numpy_exp(ctx):
+    """`exponential` on the device equals the host model of numpy's SVML
+    exp (tests/test_exp_model.py pins that model to np.exp) bit-for-bit."""
+    from tools.exp_model import exp_model
+    rng = np.random.default_rng(3)
+    x = np.concatenate([rng.uniform(-40, 0, 4000), rng.uniform(-700, 700, 4000),
+                        rng.uniform(-1e-15, 1e-15, 1000),
+                        [0.0, -0.0, np.inf, -np.inf, 709.78, 709.79, -745.2, -800.0]])
+    n = x.size
+    fn = dialect.parse_function(
+        f"func @t(%a: tensor<{n}xf32>) -> tensor<{n}xf32> {{\n"
+        f"  %e = exponential %a : tensor<{n}xf32>\n  return %e : tensor<{n}xf32>\n}}\n")
+    (got,), = run_once(ctx, [fn], [[x]])
+    with np.errstate(all="ignore"):
+        want = exp_model(x)
+    assert np.array_equal(got, want), np.nonzero(got != want)[0][:10]

@@ -1,0 +1,80 @@
+"""Host model of csrc/exp_np.cuh (SVML __svml_exp8_ha restated), built as a
+tiny C helper at test time (TEST TOOL).  Same constants, same operation
+order; compiled with -frounding-math so the round-toward-zero FMA is real."""
+import ctypes
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+
+TOP = [4607182418800017408, 4607381810190059791, 4607590029391122811, 4607807467243790904, 4608034531892639509, 4608271649552348194, 4608519265307732519, 4608777843949196329, 4609047870845172685, 4609329852853191047, 4609624319271280859, 4609931822831497360, 4610252940737434541, 4610588275747672732, 4610938457307194503, 4611304142728892634]
+TAIL = [0, 4366128403083131757, 13582886257094398792, 4365834109879625876, 4360414030434708406, 4361066948569222253, 4356828907110576048, 4364097860734309385, 13588402342996091432, 13581505024848930077, 4363345029737015988, 4355455812241575463, 4362891239881388935, 4355946959017544883, 4356286533989107623, 13587350259894555120]
+C = {'100': 4609176140021203710, '140': 4825607000727502832, '180': 4604418534313441775, '1c0': 4358002977218854975, '200': 13835058055282163711, '240': 4564188319613979652, '280': 4575956411980342720, '2c0': 4586165628304189694, '300': 4595172819764221746, '340': 4602678819172700168, '380': 4607182418800017264, '3c0': 9223372036854775807, '400': 4649436239625911876, '440': 4318952042648305664}
+
+_SRC = r"""
+#include <math.h>
+#include <fenv.h>
+#include <stdint.h>
+#include <string.h>
+static const uint64_t TOP[16] = {%s};
+static const uint64_t TAIL[16] = {%s};
+static double d(uint64_t u) { double x; memcpy(&x, &u, 8); return x; }
+static uint64_t b(double x) { uint64_t u; memcpy(&u, &x, 8); return u; }
+static double scalef(double a, double kd) {
+  int e = (int)floor(kd);
+  if (e >= -1022 && e <= 1023) return a * d((uint64_t)(e + 1023) << 52);
+  if (e < -1022) { double t = a * d((uint64_t)(e + 200 + 1023) << 52); return t * d((uint64_t)(1023 - 200) << 52); }
+  double t = a * d((uint64_t)(e - 200 + 1023) << 52); return t * d((uint64_t)(200 + 1023) << 52);
+}
+double exp_np(double x) {
+  if (x != x) return x;
+  if (x > 709.782712893384) return INFINITY;
+  if (x < -745.1332191019412) return 0.0;
+  fesetround(FE_TOWARDZERO);
+  double t = fma(x, d(%sULL), d(%sULL));
+  fesetround(FE_TONEAREST);
+  double kd = t - d(%sULL);
+  int j = (int)(b(t) & 15);
+  double r = fma(-kd, d(%sULL), x);
+  r = fma(-d(%sULL), kd, r);
+  r = d(b(r) & %sULL);
+  double r2 = r * r;
+  double p = fma(d(%sULL), r, d(%sULL));
+  double q = fma(d(%sULL), r, d(%sULL));
+  double s = fma(d(%sULL), r, d(%sULL));
+  p = fma(r2, p, q);
+  p = fma(r2, p, s);
+  double u = fma(p, r, d(TAIL[j]));
+  return scalef(fma(d(TOP[j]), u, d(TOP[j])), kd);
+}
+void exp_np_vec(const double* x, double* y, long n) { for (long i = 0; i < n; i++) y[i] = exp_np(x[i]); }
+"""
+
+_lib = None
+
+
+def _build():
+    global _lib
+    if _lib is not None:
+        return _lib
+    h = lambda u: "0x%016x" % u
+    src = _SRC % (", ".join(h(x) + "ULL" for x in TOP), ", ".join(h(x) + "ULL" for x in TAIL),
+                  *[h(C[k]) for k in ("100", "140", "140", "180", "1c0", "200",
+                                      "240", "280", "2c0", "300", "340", "380")])
+    d = tempfile.mkdtemp()
+    c, so = os.path.join(d, "e.c"), os.path.join(d, "e.so")
+    open(c, "w").write(src)
+    subprocess.check_call(["gcc", "-O1", "-frounding-math", "-ffp-contract=off",
+                           "-shared", "-fPIC", c, "-o", so, "-lm"])
+    _lib = ctypes.CDLL(so)
+    return _lib
+
+
+def exp_model(x):
+    lib = _build()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    P = ctypes.POINTER(ctypes.c_double)
+    lib.exp_np_vec(x.ctypes.data_as(P), y.ctypes.data_as(P), ctypes.c_long(x.size))
+    return y
