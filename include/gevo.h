@@ -22,6 +22,8 @@
  *                                   crowding_distance :123-140
  *   gevo_nsga2_select            -- select_survivors (search.py:163-179)
  *   gevo_last_error              -- (Python exceptions in the reference)
+ *   gevo_profile                 -- (no analogue: per-instruction-class
+ *                                   cycle counters for diagnostics)
  *   gevo_last_kernel_ms          -- (no analogue: device time of the last
  *                                   gevo_eval launch, CUDA events on the
  *                                   context's stream)
@@ -118,6 +120,13 @@ int gevo_nsga2_rank(gevo_ctx* ctx, const double* cost, const double* error,
 int gevo_nsga2_select(gevo_ctx* ctx, const double* cost, const double* error,
                       int n, int keep, int32_t* chosen, int32_t* rank,
                       double* crowding);
+
+/* instruction-class profile (diagnostics): with enable != 0 the following
+ * gevo_eval calls accumulate, per class (op*16+sub)*2+big, the CTA cycles
+ * spent and the count, into GEVO_PROFILE_SLOTS (cycles, count) pairs; `out`
+ * (n int64, may be null) receives the last accumulation. */
+#define GEVO_PROFILE_SLOTS 256
+int gevo_profile(gevo_ctx* ctx, int enable, int64_t* out, int n);
 
 /* device milliseconds of the evaluation kernel of the last gevo_eval */
 int gevo_last_kernel_ms(gevo_ctx* ctx, double* ms);

@@ -6,6 +6,11 @@
  * the instruction table for its @train_step (step 0 / steps >= 1, which can
  * differ only in operand layouts) and its @forward, plus its arena size.
  *
+ * Scratch is two-tier: values small enough live in the CTA's shared memory
+ * (GEVO_BUF_SMEM, reused by liveness), the rest in the individual's HBM arena
+ * (GEVO_BUF_ARENA); a value produced by one instruction and consumed by the
+ * next therefore never round-trips through L2 unless it is large.
+ *
  * Every device element is one 64-bit word (f32 of the dialect is computed as
  * float64 exactly like the reference, ir.py:33-37; i32 -> int64; i1 -> int64
  * 0/1).  Operands address a buffer (see GEVO_BUF_*) at an element offset with
@@ -29,7 +34,8 @@ enum {
   GEVO_BUF_CONST = 1,               /* per-individual constant pool */
   GEVO_BUF_PARAM0 = 2,              /* params 0..7 -> ids 2..9 */
   GEVO_BUF_OUT0 = 2 + GEVO_MAXP,    /* returns 0..7 -> ids 10..17 */
-  GEVO_NBUF = 2 + 2 * GEVO_MAXP
+  GEVO_BUF_SMEM = 2 + 2 * GEVO_MAXP, /* per-individual scratch in shared memory */
+  GEVO_NBUF = 3 + 2 * GEVO_MAXP
 };
 
 /* element kinds */
@@ -43,8 +49,24 @@ enum {
   GEVO_OP_REDUCE = 4,  /* sub: GEVO_R_*; aux[0]=L, aux[1]=stride along axis */
   GEVO_OP_DOT = 5,     /* sub: GEVO_D_* for columns < aux[1]; aux[2] for the
                           rest; aux[0]=K */
-  GEVO_OP_PAD = 6      /* aux[d]=low[d], aux2[d]=input extent[d] */
+  GEVO_OP_PAD = 6,     /* aux[d]=low[d], aux2[d]=input extent[d] */
+  GEVO_OP_EXT = 7      /* continuation record of the preceding DOT: a fused
+                          elementwise epilogue (see below) */
 };
+
+/* Dot epilogues.  A DOT whose aux2[0] = E > 0 is followed by E GEVO_OP_EXT
+ * records.  Together they describe up to 4*E micro-ops applied, in order, to
+ * every output element before it is stored to the DOT's `out` operand:
+ *   ext.in[0..2]   extra operands, addressed with the output (i, j) index;
+ *   ext.aux[0..5], ext.aux2[0..5]: four micro-ops of three words each:
+ *     w0 = class | sub << 4 | kin << 8 | kout << 12   (class: UNARY, BINARY,
+ *          SELECT as above)
+ *     w1 = src_a | src_b << 8,  w2 = src_c
+ *   sources: 0 = the dot value, 1 + 3*e + k = operand k of ext record e,
+ *            64 + m = result of micro-op m.  The last micro-op is stored.
+ * Each micro-op rounds exactly like the standalone instruction it replaces,
+ * so fusion never changes a result bit. */
+#define GEVO_EPI_SRC_OP 64
 enum { GEVO_U_NEG = 0, GEVO_U_EXP, GEVO_U_LOG, GEVO_U_COPY, GEVO_U_CVT };
 enum {
   GEVO_B_ADD = 0, GEVO_B_SUB, GEVO_B_MUL, GEVO_B_DIV, GEVO_B_MAX,
@@ -95,7 +117,8 @@ typedef struct {
   int32_t n_weights;                  /* weight arrays (returns of train_step) */
   int32_t wofs[GEVO_MAXP];            /* offsets of each weight in the block */
   int32_t max_arena;                  /* largest arena_elems of any prog */
+  int32_t max_smem;                   /* largest shared-memory scratch (elements) */
   int64_t total_elems;                /* device elements for all individuals */
-} gevo_plan_header;
+} gevo_plan_header;                   /* 80 bytes */
 
 #endif

@@ -42,6 +42,7 @@ SIGNATURES = {
     "gevo_destroy": (ctypes.c_int, [ctypes.c_void_p]),
     "gevo_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),
     "gevo_last_kernel_ms": (ctypes.c_int, [ctypes.c_void_p, c_dblp]),
+    "gevo_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i64p, ctypes.c_int]),
     "gevo_device_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t]),
     "gevo_upload_split": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dblp,
                                          ctypes.c_int64, ctypes.c_int, c_i64p,
@@ -144,6 +145,19 @@ class Context:
                                       ctypes.byref(desc), res.ctypes.data,
                                       ptr(fw) if want_weights else None), "eval")
         return res, (fw.reshape(n_prog, weight_elems) if want_weights else None)
+
+    def profile(self, enable=True):
+        """Turn the per-instruction-class cycle counters on/off and return
+        the last accumulation as {(op, sub, big): (cycles, count)}."""
+        buf = np.zeros(512, dtype=np.int64)
+        self.check(self.lib.gevo_profile(self.h, int(enable), ptr(buf, ctypes.c_int64), 512),
+                   "profile")
+        out = {}
+        for slot in range(256):
+            cyc, cnt = int(buf[2 * slot]), int(buf[2 * slot + 1])
+            if cnt:
+                out[(slot // 2 // 16, slot // 2 % 16, slot % 2)] = (cyc, cnt)
+        return out
 
     def last_kernel_ms(self) -> float:
         ms = ctypes.c_double()

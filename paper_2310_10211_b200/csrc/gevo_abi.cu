@@ -55,6 +55,8 @@ struct gevo_ctx {
   DevBuf plan, arena, results, finalw, params, outs, ns;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
+  bool profile = false;
+  DevBuf prof;
 };
 
 static int fail(gevo_ctx* c, int code, const std::string& msg) {
@@ -87,6 +89,8 @@ int parse_plan(gevo_ctx* ctx, const void* plan, size_t bytes, PlanView* v) {
     return fail(ctx, GEVO_E_ARG, "bad plan magic/version");
   if (h->n_instr < 0 || h->n_prog < 0 || h->n_const < 0 || h->total_elems < 0)
     return fail(ctx, GEVO_E_ARG, "negative plan counts");
+  if (h->max_smem < 0 || h->max_smem > 24576)
+    return fail(ctx, GEVO_E_ARG, "shared-memory scratch exceeds 192 KB");
   size_t need = sizeof(gevo_plan_header) + (size_t)h->n_instr * sizeof(gevo_instr) +
                 (size_t)h->n_prog * sizeof(gevo_prog) + (size_t)h->n_const * 8;
   if (need != bytes) return fail(ctx, GEVO_E_ARG, "plan size mismatch");
@@ -295,6 +299,13 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   a.y_elems = (int64_t)sc.batch * sc.classes;
   a.results = static_cast<gevo_result*>(ctx->results.p);
   a.final_weights = final_weights ? static_cast<double*>(ctx->finalw.p) : nullptr;
+  a.smem_elems = h->max_smem;
+  a.prof = nullptr;
+  if (ctx->profile) {
+    if (ctx->prof.ensure(GEVO_PROFILE_SLOTS * 2 * 8)) return fail(ctx, GEVO_E_CUDA, "profile alloc");
+    CK(cudaMemsetAsync(ctx->prof.p, 0, GEVO_PROFILE_SLOTS * 2 * 8, ctx->stream));
+    a.prof = static_cast<unsigned long long*>(ctx->prof.p);
+  }
   if (a.mode == GEVO_MODE_TRAIN && a.train_nb == 0 && a.steps > 0)
     return fail(ctx, GEVO_E_ARG, "train split has no whole batch");
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -311,6 +322,17 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   ctx->last_ms = ms;
+  return GEVO_OK;
+}
+
+int gevo_profile(gevo_ctx* ctx, int enable, int64_t* out, int n) {
+  if (!ctx) return GEVO_E_ARG;
+  ctx->profile = enable != 0;
+  if (out && n > 0) {
+    if (!ctx->prof.p) { memset(out, 0, (size_t)n * 8); return GEVO_OK; }
+    const int k = n < GEVO_PROFILE_SLOTS * 2 ? n : GEVO_PROFILE_SLOTS * 2;
+    CK(cudaMemcpy(out, ctx->prof.p, (size_t)k * 8, cudaMemcpyDeviceToHost));
+  }
   return GEVO_OK;
 }
 
@@ -348,6 +370,7 @@ int gevo_exec_once(gevo_ctx* ctx, const void* plan, size_t plan_bytes, const dou
   a.arena = static_cast<double*>(ctx->arena.p);
   a.params = static_cast<const double*>(ctx->params.p);
   a.outs = static_cast<double*>(ctx->outs.p);
+  a.smem_elems = h->max_smem;
   launch_once(a, h->n_prog, ctx->stream);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(outs, ctx->outs.p, out_words * 8, cudaMemcpyDeviceToHost, ctx->stream));

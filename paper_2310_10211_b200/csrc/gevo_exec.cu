@@ -19,50 +19,182 @@
 namespace gevo {
 
 constexpr int kThreads = 256;
+#ifndef GEVO_MIN_BLOCKS
+#define GEVO_MIN_BLOCKS 2   // CTAs per SM the register budget is sized for
+#endif
 constexpr int kInstrCache = 80;   // instructions staged in shared memory
+
+// a dot's fused elementwise epilogue, decoded once per instruction into
+// shared memory (gevo_plan.h, "Dot epilogues")
+constexpr int kEpiOps = 8, kEpiExt = 6;
+constexpr int kEpiPre = 2;   // epilogue operands prefetched per output element
+struct EpiDev {
+  int nops;
+  int op[kEpiOps][4];          // class, sub, kin, kout
+  int src[kEpiOps][3];
+  int next;                    // extra operands actually read
+  int fast;                    // 0 generic, 1 f64 binary chain, 2 select
+  int fsub[kEpiOps];           // fast chain: binary sub-op per micro-op
+  int fleft[kEpiOps];          // fast chain: dot value is the left operand
+  const double* ptr[kEpiExt];  // operand base + offset
+  int64_t st0[kEpiExt], st1[kEpiExt];
+};
 
 struct Shared {
   double* base[GEVO_NBUF];
   int flag;
   int wrong;
+  EpiDev epi;
 };
 
 __device__ __forceinline__ double* opptr(const Shared& S, const gevo_operand& o) {
   return S.base[o.buf];
 }
 
-// elementwise (UNARY / BINARY / SELECT) over the output shape
-__device__ void run_elementwise(const Shared& S, const gevo_instr& I) {
-  const int n = I.n;
-  const int rank = I.rank;
-  double* out = opptr(S, I.out);
-  const double* in0 = opptr(S, I.in[0]);
-  const double* in1 = I.op >= GEVO_OP_BINARY ? opptr(S, I.in[1]) : nullptr;
-  const double* in2 = I.op == GEVO_OP_SELECT ? opptr(S, I.in[2]) : nullptr;
-  const int am_out = I.aux2[0], am0 = I.aux2[1], am1 = I.aux2[2], am2 = I.aux2[3];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    int idx[GEVO_MAXR];
-    if (am_out == AM_STRIDED || am0 == AM_STRIDED || am1 == AM_STRIDED || am2 == AM_STRIDED)
-      unravel(i, rank, I.shp, idx);
-    auto ad = [&](const gevo_operand& o, int am) -> int64_t {
-      if (am == AM_LINEAR) return o.off + i;
-      if (am == AM_SCALAR) return o.off;
-      return addr(o, idx, rank);
-    };
-    double a = in0[ad(I.in[0], am0)];
-    double r;
-    if (I.op == GEVO_OP_UNARY) {
-      r = apply_unary(I.sub, I.kin, I.kout, a);
-    } else if (I.op == GEVO_OP_BINARY) {
-      r = apply_binary(I.sub, I.kin, a, in1[ad(I.in[1], am1)]);
-    } else {
-      r = as_i64(a) != 0 ? in1[ad(I.in[1], am1)] : in2[ad(I.in[2], am2)];
+// ---------------------------------------------------------------------------
+// elementwise (UNARY / BINARY / SELECT)
+//
+// The op is resolved once per instruction into a functor; the element loop
+// is then specialised per functor and per addressing class: every operand
+// linear/scalar (index math free) or some operand strided (unravel).  Each
+// thread keeps kEwUnroll independent elements in flight for memory-level
+// parallelism.
+// ---------------------------------------------------------------------------
+constexpr int kEwUnroll = 4;
+
+struct EwDesc {
+  double* out;
+  const double* in[3];
+  int64_t off[4];      // out, in0, in1, in2
+  int32_t step[4];     // linear: 1, scalar: 0 (fast path)
+  int n, rank, kin, kout, sub;
+  bool strided;
+};
+
+struct FAdd { __device__ double operator()(double a, double b, double) const { return __dadd_rn(a, b); } };
+struct FSub { __device__ double operator()(double a, double b, double) const { return __dsub_rn(a, b); } };
+struct FMul { __device__ double operator()(double a, double b, double) const { return __dmul_rn(a, b); } };
+struct FDiv { __device__ double operator()(double a, double b, double) const { return __ddiv_rn(a, b); } };
+struct FMax { __device__ double operator()(double a, double b, double) const { return np_fmax(a, b); } };
+struct FGt { __device__ double operator()(double a, double b, double) const { return as_w(a > b); } };
+struct FNeg { __device__ double operator()(double a, double, double) const { return -a; } };
+struct FExp { __device__ double operator()(double a, double, double) const { return exp_np(a); } };
+struct FCopy { __device__ double operator()(double a, double, double) const { return a; } };
+struct FSel { __device__ double operator()(double p, double t, double f) const { return as_i64(p) != 0 ? t : f; } };
+struct FBinGeneric {   // any kind / compare: runtime sub
+  int sub, kin;
+  __device__ double operator()(double a, double b, double) const { return apply_binary(sub, kin, a, b); }
+};
+struct FUnGeneric {
+  int sub, kin, kout;
+  __device__ double operator()(double a, double, double) const { return apply_unary(sub, kin, kout, a); }
+};
+
+template <int NIN, class F>
+__device__ __noinline__ void ew_linear(const EwDesc d, F f) {
+  const int bd = blockDim.x;
+  for (int base = threadIdx.x; base < d.n; base += kEwUnroll * bd) {
+    double a[kEwUnroll], b[kEwUnroll], c[kEwUnroll];
+#pragma unroll
+    for (int u = 0; u < kEwUnroll; ++u) {
+      const int i = base + u * bd;
+      if (i < d.n) {
+        a[u] = d.in[0][d.off[1] + (int64_t)i * d.step[1]];
+        if (NIN > 1) b[u] = d.in[1][d.off[2] + (int64_t)i * d.step[2]];
+        if (NIN > 2) c[u] = d.in[2][d.off[3] + (int64_t)i * d.step[3]];
+      }
     }
-    out[ad(I.out, am_out)] = r;
+#pragma unroll
+    for (int u = 0; u < kEwUnroll; ++u) {
+      const int i = base + u * bd;
+      if (i < d.n) d.out[d.off[0] + (int64_t)i * d.step[0]] = f(a[u], NIN > 1 ? b[u] : 0.0, NIN > 2 ? c[u] : 0.0);
+    }
   }
 }
 
-__device__ void run_pad(const Shared& S, const gevo_instr& I) {
+template <int NIN, class F>
+__device__ __noinline__ void ew_strided(const gevo_instr& I, const EwDesc d, F f) {
+  int32_t shp[GEVO_MAXR], st[4][GEVO_MAXR];
+  const gevo_operand* ops[4] = {&I.out, &I.in[0], &I.in[1], &I.in[2]};
+#pragma unroll
+  for (int r = 0; r < GEVO_MAXR; ++r) {
+    shp[r] = I.shp[r];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) st[k][r] = (k <= NIN) ? ops[k]->st[r] : 0;
+  }
+  const int rank = d.rank;
+  for (int i = threadIdx.x; i < d.n; i += blockDim.x) {
+    int idx[GEVO_MAXR];
+    unravel(i, rank, shp, idx);
+    int64_t ad[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int64_t v = d.off[k];
+#pragma unroll
+      for (int r = 0; r < GEVO_MAXR; ++r)
+        if (r < rank) v += (int64_t)idx[r] * st[k][r];
+      ad[k] = v;
+    }
+    const double a = d.in[0][ad[1]];
+    const double b = NIN > 1 ? d.in[1][ad[2]] : 0.0;
+    const double c = NIN > 2 ? d.in[2][ad[3]] : 0.0;
+    d.out[ad[0]] = f(a, b, c);
+  }
+}
+
+template <int NIN, class F>
+__device__ __forceinline__ void ew_run(const gevo_instr& I, const EwDesc& d, F f) {
+  if (d.strided) ew_strided<NIN>(I, d, f);
+  else ew_linear<NIN>(d, f);
+}
+
+__device__ __noinline__ void run_elementwise(const Shared& S, const gevo_instr& I) {
+  EwDesc d;
+  const int op = I.op;
+  d.n = I.n;
+  d.rank = I.rank;
+  d.kin = I.kin;
+  d.kout = I.kout;
+  d.sub = I.sub;
+  d.out = opptr(S, I.out);
+  d.off[0] = I.out.off;
+  const int nin = op == GEVO_OP_UNARY ? 1 : (op == GEVO_OP_BINARY ? 2 : 3);
+  d.strided = I.aux2[0] == AM_STRIDED;
+  d.step[0] = I.aux2[0] == AM_LINEAR ? 1 : 0;
+  for (int k = 0; k < 3; ++k) {
+    if (k < nin) {
+      d.in[k] = opptr(S, I.in[k]);
+      d.off[k + 1] = I.in[k].off;
+      d.step[k + 1] = I.aux2[k + 1] == AM_LINEAR ? 1 : 0;
+      d.strided |= I.aux2[k + 1] == AM_STRIDED;
+    } else {
+      d.in[k] = d.in[0];
+      d.off[k + 1] = 0;
+      d.step[k + 1] = 0;
+    }
+  }
+  if (op == GEVO_OP_SELECT) { ew_run<3>(I, d, FSel()); return; }
+  if (op == GEVO_OP_UNARY) {
+    if (d.sub == GEVO_U_COPY) { ew_run<1>(I, d, FCopy()); return; }
+    if (d.kin == GEVO_K_F64 && d.sub == GEVO_U_EXP) { ew_run<1>(I, d, FExp()); return; }
+    if (d.kin == GEVO_K_F64 && d.sub == GEVO_U_NEG) { ew_run<1>(I, d, FNeg()); return; }
+    ew_run<1>(I, d, FUnGeneric{d.sub, d.kin, d.kout});
+    return;
+  }
+  if (d.kin == GEVO_K_F64) {
+    switch (d.sub) {
+      case GEVO_B_ADD: ew_run<2>(I, d, FAdd()); return;
+      case GEVO_B_SUB: ew_run<2>(I, d, FSub()); return;
+      case GEVO_B_MUL: ew_run<2>(I, d, FMul()); return;
+      case GEVO_B_DIV: ew_run<2>(I, d, FDiv()); return;
+      case GEVO_B_MAX: ew_run<2>(I, d, FMax()); return;
+      case GEVO_B_GT: ew_run<2>(I, d, FGt()); return;
+    }
+  }
+  ew_run<2>(I, d, FBinGeneric{d.sub, d.kin});
+}
+
+__device__ __noinline__ void run_pad(const Shared& S, const gevo_instr& I) {
   double* out = opptr(S, I.out);
   const double* in = opptr(S, I.in[0]);
   const double pv = opptr(S, I.in[1])[I.in[1].off];
@@ -83,7 +215,7 @@ __device__ void run_pad(const Shared& S, const gevo_instr& I) {
   }
 }
 
-__device__ void run_reduce(const Shared& S, const gevo_instr& I) {
+__device__ __noinline__ void run_reduce(const Shared& S, const gevo_instr& I) {
   double* out = opptr(S, I.out);
   const double* in = opptr(S, I.in[0]);
   const int L = I.aux[0];
@@ -152,67 +284,370 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
-// FMA-chain dot over output columns [0, ncols): one warp owns an 8x16 strip
-// (two 8x8 tiles sharing the A fragment) for the whole K range -- never a
-// split-K, which would change the summation order.
-__device__ void dot_fma_dmma(const gevo_instr& I, double* out, const double* A,
-                             const double* B, int ncols) {
-  const int M = I.shp[0], K = I.aux[0];
-  const int64_t sam = I.in[0].st[0], sak = I.in[0].st[1];
-  const int64_t sbk = I.in[1].st[0], sbn = I.in[1].st[1];
-  const int64_t som = I.out.st[0], son = I.out.st[1];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int tm = (M + 7) >> 3, tn2 = (ncols + 15) >> 4;
-  const int K4 = K & ~3;
-  A += I.in[0].off;
-  B += I.in[1].off;
-  for (int tile = warp; tile < tm * tn2; tile += nwarp) {
-    const int ti = tile / tn2, tj = tile - ti * tn2;
-    const int i = ti * 8 + g;                 // A-fragment row of this lane
-    const int j0 = tj * 16 + g, j1 = j0 + 8;  // B-fragment columns of this lane
-    const bool vi = i < M, v0 = j0 < ncols, v1 = j1 < ncols;
-    const double* pa = A + (vi ? i : 0) * sam + t4 * sak;
-    const double* pb0 = B + (v0 ? j0 : 0) * sbn + t4 * sbk;
-    const double* pb1 = B + (v1 ? j1 : 0) * sbn + t4 * sbk;
-    const int64_t ska = 4 * sak, skb = 4 * sbk;
-    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
-#pragma unroll 4
-    for (int k0 = 0; k0 < K4; k0 += 4) {
-      const double a = vi ? *pa : 0.0;
-      const double b0 = v0 ? *pb0 : 0.0;
-      const double b1 = v1 ? *pb1 : 0.0;
-      dmma884(c00, c01, a, b0);
-      dmma884(c10, c11, a, b1);
-      pa += ska;
-      pb0 += skb;
-      pb1 += skb;
-    }
-    // D fragment: row ti*8+g, columns tj*16 + {2t4, 2t4+1} and +8
-    const int r = ti * 8 + g;
-    const int cA = tj * 16 + 2 * t4, cB = cA + 8;
-    if (K4 < K && r < M) {                    // k tail, same chain order
-      const double* ar = A + r * sam;
-      for (int k = K4; k < K; ++k) {
-        const double a = ar[k * sak];
-        const double* bk = B + k * sbk;
-        if (cA < ncols) c00 = fma(a, bk[cA * sbn], c00);
-        if (cA + 1 < ncols) c01 = fma(a, bk[(cA + 1) * sbn], c01);
-        if (cB < ncols) c10 = fma(a, bk[cB * sbn], c10);
-        if (cB + 1 < ncols) c11 = fma(a, bk[(cB + 1) * sbn], c11);
-      }
-    }
-    if (r < M) {
-      double* o = out + I.out.off + r * som;
-      if (cA < ncols) o[cA * son] = c00;
-      if (cA + 1 < ncols) o[(cA + 1) * son] = c01;
-      if (cB < ncols) o[cB * son] = c10;
-      if (cB + 1 < ncols) o[(cB + 1) * son] = c11;
+// FMA-chain dots (see dot_direct below) and fused epilogues.
+constexpr int kStageElems = 0;   // no staging region (direct-load dots)
+
+// decode the EXT records following a DOT (thread 0; caller syncs)
+__device__ void decode_epilogue(Shared& S, const gevo_instr* ext, int n_ext, int nops) {
+  EpiDev& e = S.epi;
+  e.nops = nops;
+  int used = 0;
+  for (int m = 0; m < nops; ++m) {
+    const gevo_instr& X = ext[m >> 2];
+    const int q = m & 3;
+    const int w0 = q < 2 ? X.aux[3 * q] : X.aux2[3 * q - 6];
+    const int w1 = q < 2 ? X.aux[3 * q + 1] : X.aux2[3 * q - 5];
+    const int w2 = q < 2 ? X.aux[3 * q + 2] : X.aux2[3 * q - 4];
+    e.op[m][0] = w0 & 15;
+    e.op[m][1] = (w0 >> 4) & 15;
+    e.op[m][2] = (w0 >> 8) & 15;
+    e.op[m][3] = (w0 >> 12) & 15;
+    e.src[m][0] = w1 & 255;
+    e.src[m][1] = (w1 >> 8) & 255;
+    e.src[m][2] = w2;
+    const int nsrc = e.op[m][0] == GEVO_OP_UNARY ? 1 : (e.op[m][0] == GEVO_OP_BINARY ? 2 : 3);
+    for (int k = 0; k < nsrc; ++k)
+      if (e.src[m][k] >= 1 && e.src[m][k] < GEVO_EPI_SRC_OP) used = max(used, e.src[m][k]);
+  }
+  e.next = used;
+  // fast paths: (1) each micro-op is an f64 add/sub/mul/div/max of the
+  // running value with ext operand m (in order); (2) one select(ext0, v, ext1)
+  // or select(ext0, ext1, v)
+  bool chain = nops <= kEpiPre;
+  for (int m = 0; m < nops && chain; ++m) {
+    const int prev = m == 0 ? 0 : GEVO_EPI_SRC_OP + m - 1;
+    chain = e.op[m][0] == GEVO_OP_BINARY && e.op[m][2] == GEVO_K_F64 && e.op[m][1] <= GEVO_B_MAX;
+    if (chain && e.src[m][0] == prev && e.src[m][1] == m + 1) e.fleft[m] = 1;
+    else if (chain && e.src[m][1] == prev && e.src[m][0] == m + 1) e.fleft[m] = 0;
+    else chain = false;
+    e.fsub[m] = e.op[m][1];
+  }
+  e.fast = chain ? 1 : 0;
+  if (!chain && nops == 1 && e.op[0][0] == GEVO_OP_SELECT && e.src[0][0] == 1 &&
+      ((e.src[0][1] == 0 && e.src[0][2] == 2) || (e.src[0][1] == 2 && e.src[0][2] == 0))) {
+    e.fast = 2;
+    e.fleft[0] = e.src[0][1] == 0;   // dot value is the "then" branch
+  }
+  for (int x = 0; x < kEpiExt; ++x) {
+    if (x < 3 * n_ext) {
+      const gevo_operand& o = ext[x / 3].in[x % 3];
+      e.ptr[x] = S.base[o.buf] + o.off;
+      e.st0[x] = o.st[0];
+      e.st1[x] = o.st[1];
+    } else {
+      e.ptr[x] = nullptr;
     }
   }
 }
 
-__device__ void run_dot(const Shared& S, const gevo_instr& I) {
+// prefetch the first kEpiPre epilogue operands of output (r, c) into ev[]
+__device__ __forceinline__ void epi_fetch(const EpiDev& e, int64_t r, int64_t c, double* ev) {
+#pragma unroll
+  for (int x = 0; x < kEpiPre; ++x)
+    ev[x] = x < e.next ? e.ptr[x][r * e.st0[x] + c * e.st1[x]] : 0.0;
+}
+
+__device__ __forceinline__ double bin_f64(int sub, double a, double b) {
+  switch (sub) {
+    case GEVO_B_ADD: return __dadd_rn(a, b);
+    case GEVO_B_SUB: return __dsub_rn(a, b);
+    case GEVO_B_MUL: return __dmul_rn(a, b);
+    case GEVO_B_DIV: return __ddiv_rn(a, b);
+    default: return np_fmax(a, b);
+  }
+}
+
+// generic epilogue: any micro-op sequence (kept out of line so the dot's
+// hot loops do not carry its registers)
+__device__ __noinline__ double epilogue_generic(const EpiDev& e, const double* ev, double v,
+                                                int64_t r, int64_t c) {
+  double vals[kEpiOps + 1];
+  vals[0] = v;
+  for (int m = 0; m < e.nops; ++m) {
+    double a[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int s = e.src[m][k];
+      if (s == 0) a[k] = vals[0];
+      else if (s >= GEVO_EPI_SRC_OP) a[k] = vals[1 + s - GEVO_EPI_SRC_OP];
+      else if (s == 1) a[k] = ev[0];
+      else if (s == 2) a[k] = ev[1];
+      else a[k] = e.ptr[s - 1][r * e.st0[s - 1] + c * e.st1[s - 1]];
+    }
+    const int cls = e.op[m][0];
+    double res;
+    if (cls == GEVO_OP_UNARY) res = apply_unary(e.op[m][1], e.op[m][2], e.op[m][3], a[0]);
+    else if (cls == GEVO_OP_BINARY) res = apply_binary(e.op[m][1], e.op[m][2], a[0], a[1]);
+    else res = as_i64(a[0]) != 0 ? a[1] : a[2];
+    vals[m + 1] = res;
+  }
+  return vals[e.nops];
+}
+
+// epilogue kinds the dot kernels are specialised for
+enum { EK_NONE = 0, EK_CHAIN = 1, EK_SELECT = 2, EK_GENERIC = 3 };
+
+// apply the decoded epilogue to dot value v at (r, c); operands below
+// kEpiPre come prefetched in ev[], the rest are loaded here
+template <int EK>
+__device__ __forceinline__ double epilogue_k(const EpiDev& e, const double* ev, double v,
+                                             int64_t r, int64_t c) {
+  if (EK == EK_NONE) return v;
+  if (EK == EK_CHAIN) {
+#pragma unroll
+    for (int m = 0; m < kEpiPre; ++m)
+      if (m < e.nops) v = e.fleft[m] ? bin_f64(e.fsub[m], v, ev[m]) : bin_f64(e.fsub[m], ev[m], v);
+    return v;
+  }
+  if (EK == EK_SELECT) {
+    const bool p = as_i64(ev[0]) != 0;
+    return e.fleft[0] ? (p ? v : ev[1]) : (p ? ev[1] : v);
+  }
+  return epilogue_generic(e, ev, v, r, c);
+}
+
+__device__ __forceinline__ double epilogue(const EpiDev& e, const double* ev, double v,
+                                           int64_t r, int64_t c) {
+  if (e.fast == 1) return epilogue_k<EK_CHAIN>(e, ev, v, r, c);
+  if (e.fast == 2) return epilogue_k<EK_SELECT>(e, ev, v, r, c);
+  return epilogue_generic(e, ev, v, r, c);
+}
+
+// Barrier-free FMA-chain dot: every warp streams its own DMMA fragments
+// straight from memory (L1/L2; shared memory for the smem arena), eight
+// k-steps (32 k) per group, with the next group's loads issued before the
+// current group's DMMAs (register double buffer).  Warp strips are 8 rows x
+// 16 columns (two 8x8 tiles sharing the A fragment); strips are dealt to
+// warps round-robin.  Out-of-range rows/columns read a clamped (valid)
+// address and are simply not stored.  Each output element is one fma chain
+// over k = 0..K-1 in order, so the result is the reference's bit for bit.
+constexpr int kGrp = 4;   // k-steps (of 4) per software-pipeline group (long K)
+constexpr int kShortK = 8; // k-steps held in registers by the short-K variant
+
+struct DotGeom {
+  const double* A;
+  const double* B;
+  double* out;
+  int64_t sam, sak, sbk, sbn, som, son;
+  int M, K, ncols;
+};
+
+template <int EK>
+__device__ __forceinline__ void dot_store4(const DotGeom& d, const EpiDev* epi, int orow,
+                                           int cA, int cB, double c00, double c01, double c10,
+                                           double c11, const double (*ev)[kEpiPre]) {
+  if (orow >= d.M) return;
+  double* o = d.out + orow * d.som;
+  if (EK != EK_NONE) {
+    c00 = epilogue_k<EK>(*epi, ev[0], c00, orow, cA);
+    c01 = epilogue_k<EK>(*epi, ev[1], c01, orow, cA + 1);
+    c10 = epilogue_k<EK>(*epi, ev[2], c10, orow, cB);
+    c11 = epilogue_k<EK>(*epi, ev[3], c11, orow, cB + 1);
+  }
+  if (cA < d.ncols) o[cA * d.son] = c00;
+  if (cA + 1 < d.ncols) o[(cA + 1) * d.son] = c01;
+  if (cB < d.ncols) o[cB * d.son] = c10;
+  if (cB + 1 < d.ncols) o[(cB + 1) * d.son] = c11;
+}
+
+template <int EK>
+__device__ __forceinline__ void epi_fetch4(const DotGeom& d, const EpiDev* epi, int orow, int cA,
+                                           int cB, double (*ev)[kEpiPre]) {
+  if (EK == EK_NONE || orow >= d.M) return;
+  if (cA < d.ncols) epi_fetch(*epi, orow, cA, ev[0]);
+  if (cA + 1 < d.ncols) epi_fetch(*epi, orow, cA + 1, ev[1]);
+  if (cB < d.ncols) epi_fetch(*epi, orow, cB, ev[2]);
+  if (cB + 1 < d.ncols) epi_fetch(*epi, orow, cB + 1, ev[3]);
+}
+
+// k tail (K % 4 remaining k) for one lane's four accumulators, in chain order
+__device__ __forceinline__ void dot_ktail(const DotGeom& d, int orow, int cA, int cB,
+                                          double& c00, double& c01, double& c10, double& c11) {
+  const int K4 = d.K & ~3;
+  if (K4 == d.K || orow >= d.M) return;
+  const double* ar = d.A + orow * d.sam;
+  for (int k = K4; k < d.K; ++k) {
+    const double a = ar[k * d.sak];
+    const double* bk = d.B + k * d.sbk;
+    if (cA < d.ncols) c00 = fma(a, bk[cA * d.sbn], c00);
+    if (cA + 1 < d.ncols) c01 = fma(a, bk[(cA + 1) * d.sbn], c01);
+    if (cB < d.ncols) c10 = fma(a, bk[cB * d.sbn], c10);
+    if (cB + 1 < d.ncols) c11 = fma(a, bk[(cB + 1) * d.sbn], c11);
+  }
+}
+
+// Long K: each warp owns strips (8 rows x 16 cols) and streams K with a
+// register double buffer of kGrp k-steps.
+template <int EK>
+__device__ __noinline__ void dot_long_k(const DotGeom d, const EpiDev* epi) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int tm = (d.M + 7) >> 3, tn = (d.ncols + 15) >> 4;
+  const int nsteps = d.K >> 2;
+  const int ngrp = nsteps / kGrp, rem = nsteps - ngrp * kGrp;
+  const int64_t ska = 4 * d.sak, skb = 4 * d.sbk;
+  for (int strip = warp; strip < tm * tn; strip += nwarp) {
+    const int ti = strip / tn, tj = strip - ti * tn;
+    const int orow = ti * 8 + g, j0 = tj * 16 + g;
+    const int cA = tj * 16 + 2 * t4, cB = cA + 8;
+    const double* pa = d.A + min(orow, d.M - 1) * d.sam + t4 * d.sak;
+    const double* pb0 = d.B + min(j0, d.ncols - 1) * d.sbn + t4 * d.sbk;
+    const double* pb1 = d.B + min(j0 + 8, d.ncols - 1) * d.sbn + t4 * d.sbk;
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+    // ping-pong register sets: the loads of group g+1 are in flight while
+    // the DMMAs of group g run; no register copies between groups (macros,
+    // not lambdas: every fragment index stays a compile-time constant)
+    double xa[kGrp], xb0[kGrp], xb1[kGrp], ya[kGrp], yb0[kGrp], yb1[kGrp];
+#define GEVO_LOAD(A_, B0_, B1_)                  \
+    {                                            \
+      _Pragma("unroll") for (int u = 0; u < kGrp; ++u) { \
+        A_[u] = pa[u * ska];                     \
+        B0_[u] = pb0[u * skb];                   \
+        B1_[u] = pb1[u * skb];                   \
+      }                                          \
+      pa += kGrp * ska;                          \
+      pb0 += kGrp * skb;                         \
+      pb1 += kGrp * skb;                         \
+    }
+#define GEVO_MMA(A_, B0_, B1_)                   \
+    {                                            \
+      _Pragma("unroll") for (int u = 0; u < kGrp; ++u) { \
+        dmma884(c00, c01, A_[u], B0_[u]);        \
+        dmma884(c10, c11, A_[u], B1_[u]);        \
+      }                                          \
+    }
+    if (ngrp > 0) GEVO_LOAD(xa, xb0, xb1);
+    int gi = 0;
+    for (; gi + 2 <= ngrp; gi += 2) {
+      GEVO_LOAD(ya, yb0, yb1);                   // group gi+1 in flight
+      GEVO_MMA(xa, xb0, xb1);                    // group gi
+      if (gi + 2 < ngrp) GEVO_LOAD(xa, xb0, xb1);  // group gi+2 in flight
+      GEVO_MMA(ya, yb0, yb1);                    // group gi+1
+    }
+    if (gi < ngrp) GEVO_MMA(xa, xb0, xb1);       // odd last group
+#undef GEVO_LOAD
+#undef GEVO_MMA
+    for (int u = 0; u < rem; ++u) {
+      dmma884(c00, c01, pa[0], pb0[0]);
+      dmma884(c10, c11, pa[0], pb1[0]);
+      pa += ska;
+      pb0 += skb;
+      pb1 += skb;
+    }
+    dot_ktail(d, orow, cA, cB, c00, c01, c10, c11);
+    double ev[4][kEpiPre];
+    epi_fetch4<EK>(d, epi, orow, cA, cB, ev);
+    dot_store4<EK>(d, epi, orow, cA, cB, c00, c01, c10, c11, ev);
+  }
+}
+
+// Short K (K <= 4*kShortK): warp w keeps one column strip (tj = w % tn) and
+// its B fragments in registers for every row strip it visits; the next row
+// strip's A fragments and epilogue operands are fetched while the current
+// one's DMMAs run.
+template <int EK>
+__device__ __noinline__ void dot_short_k(const DotGeom d, const EpiDev* epi) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int tm = (d.M + 7) >> 3, tn = (d.ncols + 15) >> 4;
+  const int nsteps = d.K >> 2;
+  const int64_t ska = 4 * d.sak, skb = 4 * d.sbk;
+  const int wpc = nwarp / tn;                // warps per column strip (>= 1)
+  const int tj = warp % tn, w0 = warp / tn;
+  if (w0 >= wpc) return;
+  const int j0 = tj * 16 + g;
+  const int cA = tj * 16 + 2 * t4, cB = cA + 8;
+  double fb0[kShortK], fb1[kShortK];
+  {
+    const double* pb0 = d.B + min(j0, d.ncols - 1) * d.sbn + t4 * d.sbk;
+    const double* pb1 = d.B + min(j0 + 8, d.ncols - 1) * d.sbn + t4 * d.sbk;
+#pragma unroll
+    for (int u = 0; u < kShortK; ++u) {
+      fb0[u] = u < nsteps ? pb0[u * skb] : 0.0;
+      fb1[u] = u < nsteps ? pb1[u * skb] : 0.0;
+    }
+  }
+  if (w0 >= tm) return;
+  // ping-pong register sets X / Y: the next row strip's A fragments and
+  // epilogue operands load while the current strip's DMMAs and stores run
+  double xa[kShortK], ya[kShortK];
+  double xev[4][kEpiPre], yev[4][kEpiPre];
+#define GEVO_FETCH(TI, FA, EV)                                          \
+  {                                                                      \
+    const int orow_ = (TI) * 8 + g;                                      \
+    const double* pa_ = d.A + min(orow_, d.M - 1) * d.sam + t4 * d.sak;  \
+    _Pragma("unroll") for (int u = 0; u < kShortK; ++u)                  \
+      FA[u] = u < nsteps ? pa_[u * ska] : 0.0;                           \
+    epi_fetch4<EK>(d, epi, orow_, cA, cB, EV);                           \
+  }
+#define GEVO_FINISH(TI, FA, EV)                                         \
+  {                                                                      \
+    const int orow_ = (TI) * 8 + g;                                      \
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;                   \
+    _Pragma("unroll") for (int u = 0; u < kShortK; ++u) {                \
+      if (u < nsteps) {                                                  \
+        dmma884(c00, c01, FA[u], fb0[u]);                                \
+        dmma884(c10, c11, FA[u], fb1[u]);                                \
+      }                                                                  \
+    }                                                                    \
+    dot_ktail(d, orow_, cA, cB, c00, c01, c10, c11);                     \
+    dot_store4<EK>(d, epi, orow_, cA, cB, c00, c01, c10, c11, EV);       \
+  }
+  GEVO_FETCH(w0, xa, xev);
+  for (int ti = w0; ti < tm; ti += 2 * wpc) {
+    const int t1 = ti + wpc, t2 = ti + 2 * wpc;
+    if (t1 < tm) GEVO_FETCH(t1, ya, yev);
+    GEVO_FINISH(ti, xa, xev);
+    if (t1 >= tm) break;
+    if (t2 < tm) GEVO_FETCH(t2, xa, xev);
+    GEVO_FINISH(t1, ya, yev);
+  }
+#undef GEVO_FETCH
+#undef GEVO_FINISH
+}
+
+__device__ void dot_direct(const gevo_instr& I, double* out, const double* A,
+                           const double* B, int ncols, const EpiDev* epi) {
+  DotGeom d;
+  d.M = I.shp[0];
+  d.K = I.aux[0];
+  d.ncols = ncols;
+  d.sam = I.in[0].st[0];
+  d.sak = I.in[0].st[1];
+  d.sbk = I.in[1].st[0];
+  d.sbn = I.in[1].st[1];
+  d.som = I.out.st[0];
+  d.son = I.out.st[1];
+  d.A = A + I.in[0].off;
+  d.B = B + I.in[1].off;
+  d.out = out + I.out.off;
+  const int tn = (ncols + 15) >> 4;
+  const int ek = !epi ? EK_NONE : (epi->fast == 1 ? EK_CHAIN : (epi->fast == 2 ? EK_SELECT : EK_GENERIC));
+  if (d.K <= 4 * kShortK + 3 && tn <= (int)(blockDim.x >> 5)) {
+    switch (ek) {
+      case EK_NONE: dot_short_k<EK_NONE>(d, epi); break;
+      case EK_CHAIN: dot_short_k<EK_CHAIN>(d, epi); break;
+      case EK_SELECT: dot_short_k<EK_SELECT>(d, epi); break;
+      default: dot_short_k<EK_GENERIC>(d, epi); break;
+    }
+  } else {
+    switch (ek) {
+      case EK_NONE: dot_long_k<EK_NONE>(d, epi); break;
+      case EK_CHAIN: dot_long_k<EK_CHAIN>(d, epi); break;
+      case EK_SELECT: dot_long_k<EK_SELECT>(d, epi); break;
+      default: dot_long_k<EK_GENERIC>(d, epi); break;
+    }
+  }
+}
+
+__device__ __noinline__ void run_dot(Shared& S, const gevo_instr& I, double* stage) {
+  const int n_ext = I.aux2[0];
+  const EpiDev* epi = nullptr;
+  if (n_ext > 0) {
+    if (threadIdx.x == 0) decode_epilogue(S, &I + 1, n_ext, I.aux2[1]);
+    __syncthreads();
+    epi = &S.epi;
+  }
   double* out = opptr(S, I.out);
   const double* A = opptr(S, I.in[0]);
   const double* B = opptr(S, I.in[1]);
@@ -223,7 +658,7 @@ __device__ void run_dot(const Shared& S, const gevo_instr& I) {
   const bool f = I.kin == GEVO_K_F64;
   int first = 0;  // columns [0, first) done on the tensor path
   if (f && I.sub == GEVO_D_FMA_CHAIN && split > 0) {
-    dot_fma_dmma(I, out, A, B, split);
+    dot_direct(I, out, A, B, split, epi);
     first = split;
     if (first >= N) return;
   }
@@ -241,11 +676,25 @@ __device__ void run_dot(const Shared& S, const gevo_instr& I) {
         acc += (uint64_t)as_i64(a[k * sak]) * (uint64_t)as_i64(b[k * sbk]);
       r = as_w((int64_t)acc);
     }
+    if (epi) {
+      double evs[kEpiPre];
+      epi_fetch(*epi, i, j, evs);
+      r = epilogue(*epi, evs, r, i, j);
+    }
     out[I.out.off + (int64_t)i * I.out.st[0] + (int64_t)j * I.out.st[1]] = r;
   }
 }
 
-__device__ void run_instrs(const Shared& S, const gevo_instr* ins, int n) {
+// profile slot of an instruction: op class x sub-op x size bucket
+__device__ __forceinline__ int prof_slot(const gevo_instr& I) {
+  const int big = I.n >= 4096 ? 1 : 0;
+  return ((I.op & 7) * 16 + (I.sub & 15)) * 2 + big;
+}
+
+__device__ void run_instrs(Shared& S, const gevo_instr* ins, int n, double* stage,
+                           unsigned long long* prof) {
+  long long t0 = 0;
+  if (prof && threadIdx.x == 0) t0 = clock64();
   for (int k = 0; k < n; ++k) {
     const gevo_instr& I = ins[k];
     switch (I.op) {
@@ -253,10 +702,17 @@ __device__ void run_instrs(const Shared& S, const gevo_instr* ins, int n) {
       case GEVO_OP_BINARY:
       case GEVO_OP_SELECT: run_elementwise(S, I); break;
       case GEVO_OP_REDUCE: run_reduce(S, I); break;
-      case GEVO_OP_DOT: run_dot(S, I); break;
+      case GEVO_OP_DOT: run_dot(S, I, stage); k += I.aux2[0]; break;
       case GEVO_OP_PAD: run_pad(S, I); break;
     }
     __syncthreads();
+    if (prof && threadIdx.x == 0) {
+      const long long t1 = clock64();
+      const int slot = prof_slot(I);
+      atomicAdd(prof + 2 * slot, (unsigned long long)(t1 - t0));
+      atomicAdd(prof + 2 * slot + 1, 1ULL);
+      t0 = t1;
+    }
   }
 }
 
@@ -277,10 +733,13 @@ __device__ bool all_finite(const double* w, int n) {
   return !__syncthreads_or(bad);
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, GEVO_MIN_BLOCKS)
 eval_kernel(EvalArgs args) {
   __shared__ Shared S;
   __shared__ gevo_instr cache[kInstrCache];
+  extern __shared__ double dyn_smem[];
+  double* dstage = dyn_smem;                // dot staging tiles
+  double* smem_arena = dyn_smem + kStageElems;
   const gevo_prog P = args.progs[blockIdx.x];
   double* ind = args.arena + P.arena_off;
   const int wsz = (args.weight_elems + 15) & ~15;
@@ -308,6 +767,7 @@ eval_kernel(EvalArgs args) {
       const int b = s % args.train_nb;
       if (threadIdx.x == 0) {
         S.base[GEVO_BUF_ARENA] = scratch;
+        S.base[GEVO_BUF_SMEM] = smem_arena;
         S.base[GEVO_BUF_CONST] = const_cast<double*>(consts);
         for (int i = 0; i < nw; ++i) {
           S.base[GEVO_BUF_PARAM0 + i] = const_cast<double*>(win) + args.wofs[i];
@@ -317,7 +777,7 @@ eval_kernel(EvalArgs args) {
         S.base[GEVO_BUF_PARAM0 + nw + 1] = const_cast<double*>(args.train_y) + (int64_t)b * args.y_elems;
       }
       __syncthreads();
-      run_instrs(S, cur, (s == 0) ? P.train0_n : P.train1_n);
+      run_instrs(S, cur, (s == 0) ? P.train0_n : P.train1_n, dstage, args.prof);
       steps_run = s + 1;
       if ((s + 1) % check == 0 && !all_finite(wout, args.weight_elems)) {
         status = GEVO_STATUS_NONFINITE_WEIGHTS;
@@ -337,6 +797,7 @@ eval_kernel(EvalArgs args) {
     for (int b = 0; b < args.score_nb; ++b) {
       if (threadIdx.x == 0) {
         S.base[GEVO_BUF_ARENA] = scratch;
+        S.base[GEVO_BUF_SMEM] = smem_arena;
         S.base[GEVO_BUF_CONST] = const_cast<double*>(consts);
         for (int i = 0; i < nw; ++i)
           S.base[GEVO_BUF_PARAM0 + i] = const_cast<double*>(final_w) + args.wofs[i];
@@ -345,7 +806,7 @@ eval_kernel(EvalArgs args) {
         S.wrong = 0;
       }
       __syncthreads();
-      run_instrs(S, fw, P.fwd_n);
+      run_instrs(S, fw, P.fwd_n, dstage, args.prof);
       if (!all_finite(probs, B * C)) { status = GEVO_STATUS_NONFINITE_PROBS; break; }
       // first-max argmax per row (np.argmax) vs label
       for (int r = threadIdx.x; r < B; r += blockDim.x) {
@@ -375,13 +836,17 @@ eval_kernel(EvalArgs args) {
 }
 
 // run one function once per prog with explicit params (tests, tools)
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, GEVO_MIN_BLOCKS)
 exec_once_kernel(OnceArgs args) {
   __shared__ Shared S;
   __shared__ gevo_instr cache[kInstrCache];
+  extern __shared__ double dyn_smem[];
+  double* dstage = dyn_smem;                // dot staging tiles
+  double* smem_arena = dyn_smem + kStageElems;
   const gevo_prog P = args.progs[blockIdx.x];
   if (threadIdx.x == 0) {
     S.base[GEVO_BUF_ARENA] = args.arena + P.arena_off;
+    S.base[GEVO_BUF_SMEM] = smem_arena;
     S.base[GEVO_BUF_CONST] = const_cast<double*>(args.consts) + P.const_off;
     for (int i = 0; i < GEVO_MAXP; ++i) {
       S.base[GEVO_BUF_PARAM0 + i] = const_cast<double*>(args.params) + P.param_off[i];
@@ -390,15 +855,19 @@ exec_once_kernel(OnceArgs args) {
   }
   __syncthreads();
   const gevo_instr* ins = stage(cache, args.instrs + P.train0, P.train0_n);
-  run_instrs(S, ins, P.train0_n);
+  run_instrs(S, ins, P.train0_n, dstage, nullptr);
 }
 
 void launch_eval(const EvalArgs& a, int n_prog, cudaStream_t st) {
-  eval_kernel<<<n_prog, kThreads, 0, st>>>(a);
+  const size_t smem = (size_t)(a.smem_elems + kStageElems) * sizeof(double);
+  cudaFuncSetAttribute(eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  eval_kernel<<<n_prog, kThreads, smem, st>>>(a);
 }
 
 void launch_once(const OnceArgs& a, int n_prog, cudaStream_t st) {
-  exec_once_kernel<<<n_prog, kThreads, 0, st>>>(a);
+  const size_t smem = (size_t)(a.smem_elems + kStageElems) * sizeof(double);
+  cudaFuncSetAttribute(exec_once_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  exec_once_kernel<<<n_prog, kThreads, smem, st>>>(a);
 }
 
 }  // namespace gevo

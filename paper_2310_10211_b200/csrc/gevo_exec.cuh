@@ -24,6 +24,8 @@ struct EvalArgs {
   int64_t x_elems, y_elems;   // per batch
   gevo_result* results;
   double* final_weights;      // nullable
+  int smem_elems;             // shared-memory scratch tier per CTA
+  unsigned long long* prof;   // nullable: per-instruction-class cycles
 };
 
 struct OnceArgs {
@@ -33,6 +35,7 @@ struct OnceArgs {
   double* arena;
   const double* params;
   double* outs;
+  int smem_elems;
 };
 
 void launch_eval(const EvalArgs& a, int n_prog, cudaStream_t st);

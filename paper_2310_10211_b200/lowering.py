@@ -32,9 +32,18 @@ from .dialect import kind_name
 # --- constants mirrored from include/gevo_plan.h ----------------------------
 MAXR, MAXP = 6, 8
 BUF_ARENA, BUF_CONST, BUF_PARAM0, BUF_OUT0 = 0, 1, 2, 2 + MAXP
+BUF_SMEM = 2 + 2 * MAXP
+# shared-memory tier of the scratch arena (elements): values up to
+# SMEM_VALUE_MAX elements are placed there while the per-function total
+# stays within SMEM_BUDGET; everything else goes to the HBM arena.
+SMEM_VALUE_MAX = 4096
+SMEM_BUDGET = 6144
 K_F64, K_I64, K_I1 = 0, 1, 2
 KIND = {"f32": K_F64, "i32": K_I64, "i1": K_I1}
-OP_UNARY, OP_BINARY, OP_SELECT, OP_REDUCE, OP_DOT, OP_PAD = 1, 2, 3, 4, 5, 6
+OP_UNARY, OP_BINARY, OP_SELECT, OP_REDUCE, OP_DOT, OP_PAD, OP_EXT = 1, 2, 3, 4, 5, 6, 7
+EPI_SRC_OP = 64
+EPI_MAX_OPS = 8        # micro-ops fused into one dot epilogue
+EPI_MAX_EXT = 6        # extra operands (3 per continuation record)
 U_NEG, U_EXP, U_LOG, U_COPY, U_CVT = range(5)
 B_CODES = {"add": 0, "subtract": 1, "multiply": 2, "divide": 3, "maximum": 4}
 CMP_CODES = {"eq": 5, "ne": 6, "lt": 7, "le": 8, "gt": 9, "ge": 10}
@@ -59,9 +68,9 @@ HEADER_DTYPE = np.dtype([
     ("magic", "<u4"), ("version", "<u4"), ("n_instr", "<i4"),
     ("n_prog", "<i4"), ("n_const", "<i4"), ("weight_elems", "<i4"),
     ("n_weights", "<i4"), ("wofs", "<i4", (MAXP,)), ("max_arena", "<i4"),
-    ("total_elems", "<i8")], align=True)
+    ("max_smem", "<i4"), ("total_elems", "<i8")], align=True)
 assert INSTR_DTYPE.itemsize == 224 and PROG_DTYPE.itemsize == 112
-assert HEADER_DTYPE.itemsize == 72
+assert HEADER_DTYPE.itemsize == 80
 
 FLAG_LAYOUT_APPROX = 1     # returned layouts did not reach a fixed point
 
@@ -89,6 +98,7 @@ class Lowered:
     arena_elems: int
     ret_strides: list            # numpy layout of each returned value
     cost: float
+    smem_elems: int = 0
 
 
 @dataclass
@@ -96,6 +106,7 @@ class _Alloc:
     size: int
     off: int = -1
     fixed: tuple | None = None   # (buf, off) when stored outside the arena
+    space: str = "g"             # "s": shared-memory tier, "g": HBM arena
 
 
 def _kind_of(ty) -> int:
@@ -355,31 +366,51 @@ class _Builder:
                    tmp.kind, tmp.alloc)
 
     # -- arena assignment ---------------------------------------------------------
-    def assign_arena(self):
-        """First-fit by liveness over the instruction list: an allocation
-        lives from the instruction that writes it to the last instruction
-        reading it, so an instruction never writes over its own operands."""
+    def assign_arena(self, smem_budget=None):
+        """First-fit by liveness over the instruction list, in two tiers.
+        An allocation lives from the instruction that writes it to the last
+        instruction reading it, so an instruction never writes over its own
+        operands.  Small allocations go to shared memory while they fit the
+        budget; the rest (and the overflow) to the HBM arena.
+        Returns (hbm_elems, smem_elems)."""
+        budget = SMEM_BUDGET if smem_budget is None else smem_budget
         created, last_read = {}, {}
         for i, ins in enumerate(self.instrs):
             a = ins["out"].alloc
             if a >= 0 and self.allocs[a].fixed is None:
                 created.setdefault(a, i)
-            for v in ins["in"]:
+            for v in ins["in"] + ins.get("ext", []):
                 if v.alloc >= 0:
                     last_read[v.alloc] = i
-        live, top = [], 0
+        tiers = {"s": ([], 0), "g": ([], 0)}
+        live = {"s": [], "g": []}
+        top = {"s": 0, "g": 0}
+
+        def place(space, size, i):
+            cur = sorted(x for x in live[space] if x[2] >= i)
+            live[space] = cur
+            pos = 0
+            for off, sz, _ in cur:
+                if pos + size <= off:
+                    break
+                pos = max(pos, off + sz)
+            return pos
+
         for a_id, i in sorted(created.items(), key=lambda kv: kv[1]):
             a = self.allocs[a_id]
-            live = sorted(x for x in live if x[2] >= i)
-            pos = 0
-            for off, size, _ in live:
-                if pos + a.size <= off:
-                    break
-                pos = max(pos, off + size)
+            until = max(i, last_read.get(a_id, i))
+            space = "g"
+            if a.size <= SMEM_VALUE_MAX and budget > 0:
+                pos = place("s", a.size, i)
+                if pos + a.size <= budget:
+                    space = "s"
+            if space == "g":
+                pos = place("g", a.size, i)
             a.off = pos
-            live.append((pos, a.size, max(i, last_read.get(a_id, i))))
-            top = max(top, pos + a.size)
-        return top
+            a.space = space
+            live[space].append((pos, a.size, until))
+            top[space] = max(top[space], pos + a.size)
+        return top["g"], top["s"]
 
 
 def _op_cost(op, tys, table):
@@ -410,8 +441,73 @@ def static_cost(fn, cost_table=None) -> float:
     return total
 
 
+def _same_view(a: Val, b: Val) -> bool:
+    return (a.buf, a.off, tuple(a.shape), tuple(a.st), a.alloc) == \
+        (b.buf, b.off, tuple(b.shape), tuple(b.st), b.alloc)
+
+
+def fuse_dot_epilogues(instrs):
+    """Fold single-use elementwise consumers into the producing DOT.
+
+    A dot result D that lives in scratch (not returned) and is read exactly
+    once, through the identity view, by an elementwise instruction R is not
+    stored: R becomes a micro-op applied to each dot output element, and the
+    fused instruction takes R's place in the sequence (R's other operands are
+    all computed by then; D's operands are SSA values nothing overwrites, and
+    scratch liveness is assigned after this pass).  Repeats along chains,
+    e.g. w1' = w1 - lr * (x^T . delta) becomes one instruction writing w1'.
+    Each micro-op rounds like the instruction it replaces (bit-identical)."""
+    while True:
+        readers = {}
+        for i, r in enumerate(instrs):
+            for k, v in enumerate(r["in"]):
+                if v.alloc >= 0:
+                    readers.setdefault(v.alloc, []).append((i, k, "in"))
+            for k, v in enumerate(r.get("ext", [])):
+                if v.alloc >= 0:
+                    readers.setdefault(v.alloc, []).append((i, k, "ext"))
+        merged = False
+        for i, d in enumerate(instrs):
+            if d["op"] != OP_DOT:
+                continue
+            out = d["out"]
+            if out.alloc < 0 or out.buf != BUF_ARENA:
+                continue                      # returned value: must be stored
+            rs = readers.get(out.alloc, [])
+            if len(rs) != 1 or rs[0][2] != "in":
+                continue
+            j, k, _ = rs[0]
+            r = instrs[j]
+            if j <= i or r["op"] not in (OP_UNARY, OP_BINARY, OP_SELECT):
+                continue
+            if not _same_view(r["in"][k], out):
+                continue
+            epi = list(d.get("epi", []))
+            ext = list(d.get("ext", []))
+            others = [w for kk, w in enumerate(r["in"]) if kk != k]
+            if len(epi) >= EPI_MAX_OPS or len(ext) + len(others) > EPI_MAX_EXT:
+                continue
+            prev = 0 if not epi else EPI_SRC_OP + len(epi) - 1
+            srcs = []
+            for kk, w in enumerate(r["in"]):
+                if kk == k:
+                    srcs.append(prev)
+                else:
+                    ext.append(w)
+                    srcs.append(len(ext))    # 1-based operand index
+            epi.append((r["op"], r["sub"], r["kin"], r["kout"], srcs))
+            new = dict(d)
+            new["epi"], new["ext"], new["out"] = epi, ext, r["out"]
+            instrs[j] = new
+            del instrs[i]
+            merged = True
+            break
+        if not merged:
+            return instrs
+
+
 def lower_function(fn, param_layouts=None, ret_bufs=None, ret_layout="compact",
-                   cost_table=None) -> Lowered:
+                   cost_table=None, smem_budget=None, fuse=True) -> Lowered:
     """Lower one function.  Params i live in buffer PARAM0+i with the given
     element strides (default: C order); return r is written to ret_bufs[r]
     (default: (OUT0+r, 0))."""
@@ -424,21 +520,28 @@ def lower_function(fn, param_layouts=None, ret_bufs=None, ret_layout="compact",
         ret_bufs = [(BUF_OUT0 + r, 0) for r in range(len(fn.returns))]
     b = _Builder(fn, params, ret_bufs, ret_layout, cost_table)
     ret_st = b.run(fn.returns)
-    top = b.assign_arena()
+    if fuse:
+        fuse_dot_epilogues(b.instrs)
+    top, stop = b.assign_arena(smem_budget)
     # resolve arena offsets into the operands
     instrs = []
     for rec in b.instrs:
         fixed = []
-        for v in [rec["out"]] + rec["in"]:
+        ext = rec.get("ext", [])
+        for v in [rec["out"]] + rec["in"] + ext:
             if v.alloc >= 0 and v.buf == BUF_ARENA:
                 a = b.allocs[v.alloc]
-                fixed.append(Val(BUF_ARENA, a.off + v.off, v.shape, v.st, v.kind))
+                buf = BUF_SMEM if a.space == "s" else BUF_ARENA
+                fixed.append(Val(buf, a.off + v.off, v.shape, v.st, v.kind))
             else:
                 fixed.append(v)
         rec = dict(rec)
-        rec["out"], rec["in"] = fixed[0], fixed[1:]
+        nin = len(rec["in"])
+        rec["out"], rec["in"] = fixed[0], fixed[1:1 + nin]
+        if ext:
+            rec["ext"] = fixed[1 + nin:]
         instrs.append(rec)
-    return Lowered(instrs, b.consts, top, ret_st, b.cost)
+    return Lowered(instrs, b.consts, top, ret_st, b.cost, stop)
 
 
 AM_STRIDED, AM_LINEAR, AM_SCALAR = 0, 1, 2
@@ -454,7 +557,40 @@ def _addr_mode(v, shape):
     return AM_STRIDED
 
 
+def _ext_records(rec):
+    """GEVO_OP_EXT continuation records of a fused dot (gevo_plan.h)."""
+    epi, ext = rec.get("epi", []), rec.get("ext", [])
+    n = max((len(epi) + 3) // 4, (len(ext) + 2) // 3)
+    out = []
+    for e in range(n):
+        words = []
+        for cls, sub, kin, kout, srcs in epi[4 * e:4 * e + 4]:
+            srcs = list(srcs) + [0] * (3 - len(srcs))
+            words += [cls | (sub << 4) | (kin << 8) | (kout << 12),
+                      srcs[0] | (srcs[1] << 8), srcs[2]]
+        words += [0] * (12 - len(words))
+        ops = ext[3 * e:3 * e + 3]
+        out.append({"op": OP_EXT, "sub": 0, "kout": 0, "kin": 0, "rank": 2, "n": 0,
+                    "shp": [1] * MAXR, "aux": words[:6], "aux2": words[6:],
+                    "out": Val(0, 0, (), (), 0), "in": ops, "n_epi": len(epi)})
+    return out
+
+
 def encode_instrs(instrs, const_base=0) -> np.ndarray:
+    flat = []
+    for rec in instrs:
+        if rec.get("epi"):
+            exts = _ext_records(rec)
+            rec = dict(rec)
+            aux2 = list(rec["aux2"])
+            aux2[0] = len(exts)
+            aux2[1] = len(rec["epi"])
+            rec["aux2"] = aux2
+            flat.append(rec)
+            flat.extend(exts)
+        else:
+            flat.append(rec)
+    instrs = flat
     arr = np.zeros(len(instrs), dtype=INSTR_DTYPE)
     for i, rec in enumerate(instrs):
         e = arr[i]

@@ -26,6 +26,7 @@ class VariantPlan:
     fwd: list
     consts: list
     arena: int
+    smem: int
     flags: int
     train_cost: float
     fwd_cost: float
@@ -45,6 +46,7 @@ def lower_variant(functions: dict, cost_table=None, training=True,
     constants; steps >= 1 see the layout the previous step stored."""
     consts: list = []
     arena = 0
+    smem = 0
     flags = 0
     t0 = t1 = None
     train_cost = 0.0
@@ -70,6 +72,7 @@ def lower_variant(functions: dict, cost_table=None, training=True,
         t0 = _shift_consts(low0, consts)
         t1 = t0 if low1 is low0 else _shift_consts(low1, consts)
         arena = max(low0.arena_elems, low1.arena_elems)
+        smem = max(low0.smem_elems, low1.smem_elems)
         fwd_layouts = list(low1.ret_strides)
     fw = functions["forward"]
     nwf = len(fw.params) - 1
@@ -79,7 +82,8 @@ def lower_variant(functions: dict, cost_table=None, training=True,
     lowf = lower_function(fw, f_layout, ret_layout="c", cost_table=cost_table)
     f = _shift_consts(lowf, consts)
     arena = max(arena, lowf.arena_elems)
-    return VariantPlan(t0, t1, f, consts, arena, flags, train_cost, lowf.cost)
+    smem = max(smem, lowf.smem_elems)
+    return VariantPlan(t0, t1, f, consts, arena, smem, flags, train_cost, lowf.cost)
 
 
 def _shift_consts(low, pool):
@@ -93,6 +97,8 @@ def _shift_consts(low, pool):
     for rec in low.instrs:
         rec = dict(rec)
         rec["in"] = [_rebase(v, base) for v in rec["in"]]
+        if rec.get("ext"):
+            rec["ext"] = [_rebase(v, base) for v in rec["ext"]]
         out.append(rec)
     return out
 
@@ -129,6 +135,7 @@ def build_population_plan(variants: list[VariantPlan], weight_shapes,
     n_instr = n_const = 0
     elem = 0
     max_arena = 0
+    max_smem = 0
     for slot, idx in enumerate(order):
         v = variants[idx]
         p = progs[slot]
@@ -157,6 +164,7 @@ def build_population_plan(variants: list[VariantPlan], weight_shapes,
         p["arena_elems"] = arena
         p["flags"] = v.flags
         max_arena = max(max_arena, arena)
+        max_smem = max(max_smem, v.smem)
         # [scratch | probs | weights ping | weights pong], 16-element aligned
         elem += arena + ((probs_elems + 15) & ~15) + 2 * ((wtotal + 15) & ~15)
     hdr = np.zeros(1, dtype=HEADER_DTYPE)
@@ -166,6 +174,7 @@ def build_population_plan(variants: list[VariantPlan], weight_shapes,
     hdr["n_weights"] = len(wsizes)
     hdr["wofs"][0, :len(wsizes)] = wofs[:-1]
     hdr["max_arena"] = max_arena
+    hdr["max_smem"] = max_smem
     hdr["total_elems"] = elem
     instrs = np.concatenate(instr_chunks) if instr_chunks else \
         np.zeros(0, dtype=INSTR_DTYPE)
@@ -187,9 +196,11 @@ def exec_once_plan(fns, param_arrays_list):
     pofs = 0
     oofs = 0
     elem = 0
+    max_smem = 0
     out_meta = []
     for i, (fn, params) in enumerate(zip(fns, param_arrays_list)):
         low = lower_function(fn, None, ret_layout="c")
+        max_smem = max(max_smem, low.smem_elems)
         a = encode_instrs(low.instrs)
         p = progs[i]
         p["train0"], p["train0_n"] = n_instr, len(a)
@@ -222,6 +233,7 @@ def exec_once_plan(fns, param_arrays_list):
     hdr = np.zeros(1, dtype=HEADER_DTYPE)
     hdr["magic"], hdr["version"] = PLAN_MAGIC, PLAN_VERSION
     hdr["n_instr"], hdr["n_prog"], hdr["n_const"] = n_instr, n, n_const
+    hdr["max_smem"] = max_smem
     hdr["total_elems"] = elem
     instrs = np.concatenate(chunks) if chunks else np.zeros(0, dtype=INSTR_DTYPE)
     consts = np.concatenate(consts_c) if consts_c else np.zeros(0)

@@ -26,7 +26,8 @@ def emulate(fn, params, param_layouts=None):
     consts = Lw.consts_to_words(low.consts).view(np.int64).copy() if low.consts \
         else np.zeros(1, dtype=np.int64)
     mem = {Lw.BUF_ARENA: np.zeros(max(low.arena_elems, 1), dtype=np.int64),
-           Lw.BUF_CONST: consts}
+           Lw.BUF_CONST: consts,
+           Lw.BUF_SMEM: np.zeros(max(low.smem_elems, 1), dtype=np.int64)}
     for k, p in enumerate(params):
         mem[Lw.BUF_PARAM0 + k] = _words(p)
     for r, ty in enumerate(fn.return_types):

@@ -1,8 +1,14 @@
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 600 python -m pytest tests -m gpu -x -q -s 2>&1 | tail -25 > gpurun_out/gpu_tests.log
-timeout 300 python __graft_entry__.py > gpurun_out/smoke.log 2>&1
-timeout 600 python bench.py --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/bench2.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:eval_kernel -s 1 -c 1 -o gpurun_out/prof_eval python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
-tail -3 gpurun_out/gpu_tests.log gpurun_out/smoke.log gpurun_out/bench2.log gpurun_out/ncu_full.log
+# one GPU round trip: parity tests, smoke, bench, ncu launch list + full capture
+# usage: bash tests/tools/gpu_run.sh [tag] [bench args...]
+TAG=${1:-run}; shift
+BENCH_ARGS=${@:---steps 3 --warmup 2 --no-cpu-baseline}
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
+timeout 900 python -m pytest tests -m gpu -x -q -s > gpurun_out/${TAG}_tests.log 2>&1
+grep -E "bit-exact|passed|failed|Error|error" gpurun_out/${TAG}_tests.log | tail -12
+timeout 300 python __graft_entry__.py > gpurun_out/${TAG}_smoke.log 2>&1; tail -n 1 gpurun_out/${TAG}_smoke.log
+timeout 900 python bench.py $BENCH_ARGS > gpurun_out/${TAG}_bench.log 2>&1; tail -n 2 gpurun_out/${TAG}_bench.log
+if [ -z "$NO_NCU" ]; then
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:eval_kernel -s 1 -c 1 -o gpurun_out/${TAG}_prof python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/${TAG}_ncu.log 2>&1
+tail -n 1 gpurun_out/${TAG}_ncu.log
+fi

@@ -1,10 +1,10 @@
 """Vectorised CPU walker of a lowered instruction table (TEST TOOL ONLY).
 
 It checks the *lowering* (addressing, view folding, layouts, arena reuse,
-return placement) independently of the GPU: it executes the records that
-lowering.lower_function produces with plain numpy arithmetic (no attempt at
-numpy's summation order), so results agree with the oracle to ~1e-12, not
-bit-exactly.  Never used by the product or the bench.
+return placement, dot-epilogue fusion) independently of the GPU: it executes
+the records that lowering.lower_function produces with plain numpy
+arithmetic (no attempt at numpy's summation order), so results agree with
+the oracle to ~1e-12, not bit-exactly.  Never used by the product or bench.
 """
 from __future__ import annotations
 
@@ -39,52 +39,51 @@ def wd(x):
     return np.asarray(x, dtype=np.float64).view(np.int64)
 
 
+def ew(op, sub, kin, kout, args):
+    """One elementwise op on 64-bit word arrays."""
+    with np.errstate(all="ignore"):
+        if op == Lw.OP_SELECT:
+            p, t, f = args
+            return np.where(p != 0, t, f)
+        a = args[0]
+        if op == Lw.OP_UNARY:
+            if sub == Lw.U_COPY:
+                return a
+            if sub == Lw.U_CVT:
+                if kout == Lw.K_I1:
+                    return ((fl(a) != 0) if kin == F else (a != 0)).astype(np.int64)
+                if kout == Lw.K_I64:
+                    return np.trunc(fl(a)).astype(np.int64) if kin == F else a
+                return a if kin == F else wd(a.astype(np.float64))
+            if kin == F:
+                x = fl(a)
+                return wd({Lw.U_NEG: -x, Lw.U_EXP: np.exp(x), Lw.U_LOG: np.log(x)}[sub])
+            return -a
+        b = args[1]
+        if kin == F:
+            x, y = fl(a), fl(b)
+            if sub <= 4:
+                return wd([x + y, x - y, x * y, np.true_divide(x, y), np.maximum(x, y)][sub])
+            return [x == y, x != y, x < y, x <= y, x > y, x >= y][sub - 5].astype(np.int64)
+        if sub == 3:
+            nz = b != 0
+            q = np.trunc(np.true_divide(a, np.where(nz, b, 1)))
+            return np.where(nz, q, 0).astype(np.int64)
+        if sub <= 4:
+            return [a + b, a - b, a * b, None, np.maximum(a, b)][sub]
+        return [a == b, a != b, a < b, a <= b, a > b, a >= b][sub - 5].astype(np.int64)
+
+
 def run(instrs, mem):
     """mem: dict buf_id -> np.ndarray of int64 words (float64 bits)."""
     for rec in instrs:
         op, sub = rec["op"], rec["sub"]
         out = rec["out"]
         shape = tuple(out.shape)
-        kin, kout = rec["kin"], rec["kout"]
+        kin = rec["kin"]
         with np.errstate(all="ignore"):
-            if op == Lw.OP_SELECT:
-                p, t, f = (gather(mem, v, shape) for v in rec["in"])
-                r = np.where(p != 0, t, f)
-            elif op == Lw.OP_UNARY:
-                a = gather(mem, rec["in"][0], shape)
-                if sub == Lw.U_COPY:
-                    r = a
-                elif sub == Lw.U_CVT:
-                    if kout == Lw.K_I1:
-                        r = ((fl(a) != 0) if kin == F else (a != 0)).astype(np.int64)
-                    elif kout == Lw.K_I64:
-                        r = np.trunc(fl(a)).astype(np.int64) if kin == F else a
-                    else:
-                        r = a if kin == F else wd(a.astype(np.float64))
-                elif kin == F:
-                    x = fl(a)
-                    r = wd({Lw.U_NEG: -x, Lw.U_EXP: np.exp(x), Lw.U_LOG: np.log(x)}[sub])
-                else:
-                    r = -a
-            elif op == Lw.OP_BINARY:
-                a = gather(mem, rec["in"][0], shape)
-                b = gather(mem, rec["in"][1], shape)
-                if kin == F:
-                    x, y = fl(a), fl(b)
-                    if sub <= 4:
-                        r = wd([x + y, x - y, x * y, np.true_divide(x, y),
-                                np.maximum(x, y)][sub])
-                    else:
-                        r = [x == y, x != y, x < y, x <= y, x > y, x >= y][sub - 5].astype(np.int64)
-                else:
-                    if sub == 3:
-                        nz = b != 0
-                        q = np.trunc(np.true_divide(a, np.where(nz, b, 1)))
-                        r = np.where(nz, q, 0).astype(np.int64)
-                    elif sub <= 4:
-                        r = [a + b, a - b, a * b, None, np.maximum(a, b)][sub]
-                    else:
-                        r = [a == b, a != b, a < b, a <= b, a > b, a >= b][sub - 5].astype(np.int64)
+            if op in (Lw.OP_UNARY, Lw.OP_BINARY, Lw.OP_SELECT):
+                r = ew(op, sub, kin, rec["kout"], [gather(mem, v, shape) for v in rec["in"]])
             elif op == Lw.OP_REDUCE:
                 L, rs = rec["aux"][0], rec["aux"][1]
                 base = offsets(rec["in"][0], shape)
@@ -100,14 +99,29 @@ def run(instrs, mem):
                 M, N, K = shape[0], shape[1], rec["aux"][0]
                 A = gather(mem, a, (M, K)).reshape(M, K)
                 B = gather(mem, b, (K, N)).reshape(K, N)
-                r = wd(fl(A) @ fl(B)) if kin == F else A @ B
+                r = (wd(fl(A) @ fl(B)) if kin == F else A @ B).reshape(-1)
+                if rec.get("epi"):
+                    ext = [gather(mem, v, shape) for v in rec["ext"]]
+                    vals = [r]
+                    for cls, esub, ekin, ekout, srcs in rec["epi"]:
+                        nin = {Lw.OP_UNARY: 1, Lw.OP_BINARY: 2, Lw.OP_SELECT: 3}[cls]
+                        args = []
+                        for s in srcs[:nin]:
+                            if s == 0:
+                                args.append(vals[0])
+                            elif s >= Lw.EPI_SRC_OP:
+                                args.append(vals[1 + s - Lw.EPI_SRC_OP])
+                            else:
+                                args.append(ext[s - 1])
+                        vals.append(ew(cls, esub, ekin, ekout, args))
+                    r = vals[-1]
             elif op == Lw.OP_PAD:
                 a, pv = rec["in"]
-                low, ext = rec["aux"][:len(shape)], rec["aux2"][:len(shape)]
-                src = gather(mem, a, tuple(ext)).reshape(ext)
+                low, ext_ = rec["aux"][:len(shape)], rec["aux2"][:len(shape)]
+                src = gather(mem, a, tuple(ext_)).reshape(ext_)
                 pval = mem[pv.buf][pv.off]
                 full = np.full(shape, pval, dtype=np.int64)
-                full[tuple(slice(l, l + e) for l, e in zip(low, ext))] = src
+                full[tuple(slice(l, l + e) for l, e in zip(low, ext_))] = src
                 r = full
             else:
                 raise ValueError(f"unknown op {op}")
