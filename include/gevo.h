@@ -20,6 +20,7 @@
  *   gevo_nsga2_rank              -- rank_population (search.py:143-150):
  *                                   nondominated_sort :96-120 +
  *                                   crowding_distance :123-140
+ *   gevo_nsga2_crowding          -- crowding_distance (search.py:123-140)
  *   gevo_nsga2_select            -- select_survivors (search.py:163-179)
  *   gevo_last_error              -- (Python exceptions in the reference)
  *   gevo_profile                 -- (no analogue: per-instruction-class
@@ -114,6 +115,11 @@ int gevo_nsga2_rank(gevo_ctx* ctx, const double* cost, const double* error,
                     int n, int32_t* rank, double* crowding,
                     int32_t* front_order, int32_t* front_start,
                     int32_t* n_fronts);
+
+/* crowding_distance (search.py:123-140) of points taken as ONE front
+ * (ties on an axis break by position) */
+int gevo_nsga2_crowding(gevo_ctx* ctx, const double* cost, const double* error,
+                        int n, double* crowding);
 
 /* indices chosen by select_survivors(pool, keep) in survivor order, plus the
  * rank/crowding it assigns (search.py:163-179) */

@@ -56,6 +56,8 @@ SIGNATURES = {
                                       c_dblp, ctypes.c_size_t]),
     "gevo_nsga2_rank": (ctypes.c_int, [ctypes.c_void_p, c_dblp, c_dblp, ctypes.c_int,
                                        c_i32p, c_dblp, c_i32p, c_i32p, c_i32p]),
+    "gevo_nsga2_crowding": (ctypes.c_int, [ctypes.c_void_p, c_dblp, c_dblp, ctypes.c_int,
+                                           c_dblp]),
     "gevo_nsga2_select": (ctypes.c_int, [ctypes.c_void_p, c_dblp, c_dblp, ctypes.c_int,
                                          ctypes.c_int, c_i32p, c_i32p, c_dblp]),
 }
@@ -187,6 +189,14 @@ class Context:
             ctypes.byref(nf)), "nsga2_rank")
         k = nf.value
         return rank[:n], crowd[:n], order[:n], fstart[:k + 1]
+
+    def nsga2_crowding(self, cost, err):
+        cost = np.ascontiguousarray(cost, dtype=np.float64)
+        err = np.ascontiguousarray(err, dtype=np.float64)
+        crowd = np.zeros(max(cost.size, 1))
+        self.check(self.lib.gevo_nsga2_crowding(self.h, ptr(cost), ptr(err), cost.size,
+                                                ptr(crowd)), "nsga2_crowding")
+        return crowd[:cost.size]
 
     def nsga2_select(self, cost, err, keep):
         cost = np.ascontiguousarray(cost, dtype=np.float64)

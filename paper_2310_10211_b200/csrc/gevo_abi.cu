@@ -380,7 +380,8 @@ int gevo_exec_once(gevo_ctx* ctx, const void* plan, size_t plan_bytes, const dou
 
 static int nsga2_common(gevo_ctx* ctx, const double* cost, const double* error, int n,
                         int keep, int32_t* chosen, int32_t* rank, double* crowding,
-                        int32_t* front_order, int32_t* front_start, int32_t* n_fronts) {
+                        int32_t* front_order, int32_t* front_start, int32_t* n_fronts,
+                        int one_front = 0) {
   if (!ctx) return GEVO_E_ARG;
   if (n < 0 || !cost || !error) return fail(ctx, GEVO_E_ARG, "bad nsga2 arguments");
   if (n == 0) {
@@ -398,6 +399,7 @@ static int nsga2_common(gevo_ctx* ctx, const double* cost, const double* error, 
   NsArgs a;
   a.n = n;
   a.keep = keep;
+  a.one_front = one_front;
   a.c = d;
   a.e = d + n;
   a.crowd = d + 2 * (size_t)n;
@@ -435,6 +437,12 @@ int gevo_nsga2_rank(gevo_ctx* ctx, const double* cost, const double* error, int 
                     int32_t* front_start, int32_t* n_fronts) {
   return nsga2_common(ctx, cost, error, n, 0, nullptr, rank, crowding, front_order,
                       front_start, n_fronts);
+}
+
+int gevo_nsga2_crowding(gevo_ctx* ctx, const double* cost, const double* error, int n,
+                        double* crowding) {
+  return nsga2_common(ctx, cost, error, n, 0, nullptr, nullptr, crowding, nullptr, nullptr,
+                      nullptr, 1);
 }
 
 int gevo_nsga2_select(gevo_ctx* ctx, const double* cost, const double* error, int n,

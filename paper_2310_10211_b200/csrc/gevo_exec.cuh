@@ -44,6 +44,7 @@ void launch_once(const OnceArgs& a, int n_prog, cudaStream_t st);
 // NSGA-II (nsga2.cu)
 struct NsArgs {
   int n, keep;
+  int one_front;      // all points form a single front (crowding only)
   const double* c;
   const double* e;
   int32_t* rank;      // [n]

@@ -58,8 +58,15 @@ __global__ void __launch_bounds__(kNsThreads) nsga2_kernel(NsArgs a) {
   const int n = a.n;
   const double* C = a.c;
   const double* E = a.e;
+  if (a.one_front) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      a.count[j] = 0;
+      a.rank[j] = -1;
+    }
+    __syncthreads();
+  }
   // 1. dominator counts
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+  for (int j = threadIdx.x; j < n && !a.one_front; j += blockDim.x) {
     int cnt = 0;
     const double cj = C[j], ej = E[j];
     for (int i = 0; i < n; ++i) cnt += dom(C[i], E[i], cj, ej);
@@ -85,7 +92,7 @@ __global__ void __launch_bounds__(kNsThreads) nsga2_kernel(NsArgs a) {
     for (int k = threadIdx.x; k < added; k += blockDim.x) a.rank[a.order[base + k]] = f;
     __syncthreads();
     // remove this front's dominance from the rest
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    for (int j = threadIdx.x; j < n && !a.one_front; j += blockDim.x) {
       if (a.rank[j] != -1) continue;
       int d = 0;
       const double cj = C[j], ej = E[j];

@@ -54,9 +54,14 @@ def all_gather_records(local: np.ndarray, n_max: int, group=None):
     buf[0, 0] = len(local)
     buf[1:len(local) + 1] = local
     t = torch.from_numpy(buf).to(dev)
-    out = torch.empty((world, n_max + 1, RECORD_FIELDS), dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(out, t, group=group)
-    arr = out.cpu().numpy()
+    if dev.type == "cuda":
+        out = torch.empty((world, n_max + 1, RECORD_FIELDS), dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(out, t, group=group)
+        arr = out.cpu().numpy()
+    else:                               # gloo has no all_gather_into_tensor
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t, group=group)
+        arr = torch.stack(parts).numpy()
     counts = arr[:, 0, 0].astype(int)
     return arr[:, 1:, :], counts
 
@@ -68,3 +73,66 @@ def merge_shards(gathered, counts, shards):
     for r, idx in enumerate(shards):
         out[idx] = gathered[r, :counts[r]]
     return out
+
+
+STATUS_INVALID = -1
+
+
+class ShardedEvaluator:
+    """Population parallelism across ranks (one process per GPU).
+
+    Every rank calls evaluate_variants with the SAME list (the host GA is
+    replicated and seeded identically, so its patch lists agree); each rank
+    lowers and evaluates only its LPT shard on its own device, then ONE
+    all-gather of fixed-size records gives every rank every fitness.
+    `backend` is a DeviceEvaluator (or anything with the same
+    evaluate_variants(..., return_records=True) signature)."""
+
+    def __init__(self, backend, group=None):
+        self.backend = backend
+        self.group = group
+        self.last_shards = None
+
+    def _world(self):
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            return dist.get_world_size(self.group), dist.get_rank(self.group)
+        return 1, 0
+
+    def evaluate_variants(self, variants, holdout=False, cost_table=None):
+        from .lowering import static_cost
+        from .workloads import INVALID_FITNESS, Fitness
+        world, rank = self._world()
+        if world == 1:
+            return self.backend.evaluate_variants(variants, holdout=holdout)
+        training = "train_step" in next((v for v in variants if v), {})
+        costs = []
+        for v in variants:
+            if v is None:
+                costs.append(0.0)
+            else:
+                costs.append(static_cost(v["train_step" if training else "forward"],
+                                         cost_table))
+        shards = lpt_shards(costs, world)
+        self.last_shards = shards
+        mine = [variants[i] for i in shards[rank]]
+        fits, recs = self.backend.evaluate_variants(mine, holdout=holdout,
+                                                    return_records=True)
+        local = pack_records(fits, recs)
+        for k, f in enumerate(fits):
+            if not f.valid:
+                local[k, 3] = STATUS_INVALID
+        n_max = max(len(s) for s in shards)
+        gathered, counts = all_gather_records(local, n_max, self.group)
+        merged = merge_shards(gathered, counts, shards)
+        out = []
+        for row in merged:
+            cost = float(np.int64(row[0]).view(np.float64))
+            status = int(row[3])
+            if status == STATUS_INVALID:
+                out.append(INVALID_FITNESS)
+            elif status != 0:
+                out.append(Fitness(cost, 1.0))
+            else:
+                out.append(Fitness(cost, int(row[1]) / int(row[2])))
+        return out

@@ -1,0 +1,104 @@
+"""Population sharding over 2 ranks (gloo, CPU): LPT shards, one record
+all-gather, merged fitness identical to the single-rank result.  The device
+is replaced by the reference's recorded fitness table (see test_shims)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from golden_io import load, variant_functions
+from paper_2310_10211_b200 import distributed as D
+
+
+class TableBackend:
+    def __init__(self):
+        from paper_2310_10211_b200.dialect import format_function
+        self.fmt = format_function
+        self.table = {}
+        for ind in load("train_pop.json.gz")["individuals"]:
+            v = variant_functions(ind)
+            self.table[(format_function(v["train_step"]), format_function(v["forward"]))] = ind
+        self.seen = 0
+
+    def evaluate_variants(self, variants, holdout=False, return_records=False):
+        from paper_2310_10211_b200.workloads import Fitness, INVALID_FITNESS
+        fits = []
+        recs = np.zeros(len(variants), dtype=[("wrong", "<i8"), ("total", "<i8"),
+                                               ("status", "<i4"), ("steps_run", "<i4")])
+        for k, v in enumerate(variants):
+            if v is None:
+                fits.append(INVALID_FITNESS)
+                continue
+            ind = self.table[(self.fmt(v["train_step"]), self.fmt(v["forward"]))]
+            fits.append(Fitness(ind["cost"], ind["error"]))
+            if ind["error"] == 1.0:
+                recs[k]["status"] = 1
+            else:
+                recs[k]["wrong"] = round(ind["error"] * 992)
+                recs[k]["total"] = 992
+        self.seen += len(variants)
+        return (fits, recs) if return_records else fits
+
+
+def test_lpt_shards_cover_and_balance():
+    costs = [float(c) for c in np.random.default_rng(0).integers(1, 100, 257)]
+    for world in (1, 2, 3, 8):
+        shards = D.lpt_shards(costs, world)
+        flat = sorted(i for s in shards for i in s)
+        assert flat == list(range(len(costs)))
+        loads = [sum(costs[i] for i in s) for s in shards]
+        assert max(loads) - min(loads) <= max(costs)
+        assert all(s == sorted(s) for s in shards)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        inds = load("train_pop.json.gz")["individuals"]
+        variants = [variant_functions(i) for i in inds] + [None]
+        be = TableBackend()
+        ev = D.ShardedEvaluator(be)
+        fits = ev.evaluate_variants(variants)
+        q.put((rank, [(f.cost, f.error, f.valid) for f in fits], be.seen,
+               [len(s) for s in ev.last_shards]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gather_matches_single_rank():
+    ctx = mp.get_context("fork")      # CPU-only: no CUDA state to inherit
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    try:
+        out = [q.get(timeout=240) for _ in procs]
+    finally:
+        for p in procs:
+            if p.is_alive():
+                p.join(5)
+            if p.is_alive():
+                p.kill()
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    inds = load("train_pop.json.gz")["individuals"]
+    want = [(i["cost"], i["error"], True) for i in inds] + [(float("inf"), float("inf"), False)]
+    for rank, fits, seen, sizes in out:
+        assert fits == want                       # every rank holds every fitness
+        assert seen == sizes[rank]                # and evaluated only its shard
+    assert sum(out[0][3]) == len(want)
