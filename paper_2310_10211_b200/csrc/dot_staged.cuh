@@ -1,0 +1,818 @@
+// dot_staged.cuh -- the executor's DOT: every summation order the reference
+// can produce (lowering.dot_modes), fed through a shared-memory pipeline.
+//
+// Replaces `v[i] @ v[j]` (interpreter.py:114-116): numpy -> OpenBLAS dgemm
+// for blasable f64 operands, numpy's own loop otherwise.  Orders:
+//   FMA_CHAIN  one fma chain per output, k ascending     -> DMMA m8n8k4
+//   ACC8_TREE  8 chains (k mod 8) + fixed pairwise tree   -> DMMA per chain
+//   ACC8_TAIL  ACC8 over k < K&~7, tree, fma tail         -> DMMA + scalar tail
+//   SEQ_NOFMA  acc = acc + a*b, two roundings             -> scalar DMUL/DADD
+//   integer    wrapping int64 multiply-add                -> scalar
+// DMMA m8n8k4 was probed bit-identical to four chained fma() in k order
+// (tests/tools/dmma_probe2.cu), so a k-ordered DMMA sequence reproduces a
+// single-accumulator chain exactly; ACC8 chains get their own accumulator
+// tiles, the k values of chain j are gathered into one DMMA by a k
+// permutation applied while staging.
+//
+// Pipeline: the output is cut into panels (<= 32 x 32); each (panel, 32-k
+// chunk) is one stage: an A tile plus a second tile -- the B chunk, or, when
+// all of B fits one persistent tile, a full-matrix epilogue operand (e.g. w1
+// in w1 - lr * x^T.d) -- copied with cp.async kDotStages deep.  Each thread
+// precomputes its copy plan (source/smem offsets) once per instruction:
+// 16-byte copies along the operand's unit-stride axis when lines are
+// contiguous and aligned, 8-byte gathers for any other strides, synchronous
+// copies from the shared-memory arena.  Tile rows are padded to 36 doubles so
+// DMMA fragment reads are bank-conflict free in either orientation.
+// (A TMA bulk-copy ring -- one cp.async.bulk per 256-byte line, mbarrier
+// full/empty -- measured 2.3x slower than this ring on B200; see
+// profiles/r01_dot_experiments.md.)
+#pragma once
+#include <stdint.h>
+#include "gevo_plan.h"
+
+namespace gevo {
+
+constexpr int kKC = 32;              // k per chunk
+constexpr int kPanel = 32;           // panel rows / cols
+constexpr int kTS = 36;              // padded tile row (doubles)
+constexpr int kTileElems = kPanel * kTS;
+constexpr int kDotStages = 3;
+// 3 stages x (A tile + second tile) + one persistent B tile
+constexpr int kStageElems = (kDotStages * 2 + 1) * kTileElems;   // 8064 doubles
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+}
+// 16 bytes, of which `bytes` (8 or 16) are read and the rest zero-filled
+__device__ __forceinline__ void cp_async16(uint32_t dst, const double* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+constexpr int kDotThreads = kThreads;          // the executor's CTA
+constexpr int kDotWarps = kDotThreads / 32;
+
+constexpr int kVecPasses = 512 / kDotThreads;   // 16-byte copies per thread per tile
+constexpr int kGatherPasses = 1024 / kDotThreads;
+
+// One operand staged as 32 x 32 tiles: element (r, k) -> smem r*rs + pos(k)*ks
+// with (rs, ks) = (kTS, 1) when k is the line axis ("k-major") else (1, kTS).
+// Copies run along the line axis (the operand's unit-stride axis when it has
+// one).  Thread t's copy i covers cross index x0(t) + i*xs at line index
+// f(t): 16-byte lines (x0 = t>>4, f = 2*(t&15)) or 8-byte gathers (x0 = t>>5,
+// f = t&31).  Kept compact: this is live across the whole dot.
+enum { CP_GATHER = 0, CP_VEC = 1, CP_SMEM = 2 };
+struct CopyPlan {      // uniform across the CTA: lives in shared memory
+  const double* p;     // element (0, 0) of the operand
+  int sr, sk;          // element strides along r (m or n) and k
+  int so;              // source step between a thread's copies
+  int flags;           // bits 0-1 mode, bit 2 k-major, bit 3 ACC8 permutation
+  int cross, along;
+};
+
+__device__ __forceinline__ int cp_mode(const CopyPlan& c) { return c.flags & 3; }
+__device__ __forceinline__ bool cp_kmajor(const CopyPlan& c) { return (c.flags >> 2) & 1; }
+__device__ __forceinline__ int cp_rs(const CopyPlan& c) { return cp_kmajor(c) ? kTS : 1; }
+__device__ __forceinline__ int cp_ks(const CopyPlan& c) { return cp_kmajor(c) ? 1 : kTS; }
+
+__device__ __forceinline__ void plan_init(CopyPlan& c, const double* p, int sr, int sk, bool smem, bool perm) {
+  c.p = p;
+  c.sr = sr;
+  c.sk = sk;
+  const int ar = sr < 0 ? -sr : sr, ak = sk < 0 ? -sk : sk;
+  // lines along k when k is the (non-broadcast) contiguous axis
+  const bool kmajor = ak != 0 && (ar == 0 || ak <= ar);
+  const int cross = kmajor ? sr : sk, along = kmajor ? sk : sr;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(p) & 15) == 0) && (cross & 1) == 0;
+  const int mode = smem ? CP_SMEM : ((!perm && along == 1 && aligned) ? CP_VEC : CP_GATHER);
+  c.flags = mode | (kmajor ? 4 : 0) | (perm ? 8 : 0);
+  const int xs = mode == CP_VEC ? kDotThreads / 16 : kDotWarps;
+  c.so = xs * cross;
+  c.cross = cross;
+  c.along = along;
+}
+
+// thread's source offset of its first copy
+__device__ __forceinline__ int plan_o0(const CopyPlan& c) {
+  const int t = threadIdx.x;
+  const bool vec = (c.flags & 3) == CP_VEC;
+  const int x0 = vec ? t >> 4 : t >> 5;
+  const int f = vec ? (t & 15) * 2 : t & 31;
+  return x0 * c.cross + f * c.along;
+}
+
+// stage the tile at (r0, k0) with nr x nk valid elements into smem `dst`
+__device__ __forceinline__ void stage(uint32_t dst, const CopyPlan& c, int o0, int r0, int nr, int k0, int nk) {
+  const bool kmajor = cp_kmajor(c);
+  const int mode = cp_mode(c);
+  const int nx = kmajor ? nr : nk, nf = kmajor ? nk : nr;
+  const int t = threadIdx.x;
+  const double* src = c.p + ((int64_t)r0 * c.sr + (int64_t)k0 * c.sk + o0);
+  if (mode == CP_VEC) {
+    const int x0 = t >> 4, f = (t & 15) * 2;
+    if (f >= nf) return;
+    const int bytes = nf - f >= 2 ? 16 : 8;
+    const uint32_t d = dst + 8u * (x0 * kTS + f);
+#pragma unroll
+    for (int i = 0; i < kVecPasses; ++i)
+      if (x0 + (kDotThreads / 16) * i < nx) cp_async16(d + 8u * ((kDotThreads / 16) * kTS) * i, src + i * c.so, bytes);
+    return;
+  }
+  const int x0 = t >> 5, f = t & 31;
+  if (f >= nf) return;
+  const bool perm = (c.flags >> 3) & 1;
+  const int rs = kmajor ? kTS : 1, ks = kmajor ? 1 : kTS;
+#pragma unroll
+  for (int i = 0; i < kGatherPasses; ++i) {
+    const int x = x0 + kDotWarps * i;
+    if (x < nx) {
+      const int rr = kmajor ? x : f, kk = kmajor ? f : x;
+      const int pk = perm ? (((kk & 7) << 2) | (kk >> 3)) : kk;
+      const uint32_t d = dst + 8u * (rr * rs + pk * ks);
+      if (mode == CP_GATHER) cp_async8(d, src + i * c.so);
+      else *reinterpret_cast<double*>(__cvta_shared_to_generic(d)) = src[i * c.so];
+    }
+  }
+}
+
+// Epilogue (fused elementwise consumers of the dot, gevo_plan.h): the fast
+// kinds keep their operand descriptors in registers; each of the first
+// kEpiPre operands is a scalar, the panel's staged tile, or a direct load.
+enum { ES_SCALAR = 0, ES_TILE = 1, ES_DIRECT = 2 };
+struct EpiR {
+  int nops;
+  int src[kEpiPre], fsub[kEpiPre], fleft[kEpiPre];
+  double sval[kEpiPre];
+  const double* ptr[kEpiPre];
+  int st0[kEpiPre], st1[kEpiPre];
+  int tile;            // operand index staged with the panel (-1: none)
+};
+
+__device__ __forceinline__ void epi_init(EpiR& R, const EpiDev* e, bool tile_free) {
+  R.nops = e ? e->nops : 0;
+  R.tile = -1;
+#pragma unroll
+  for (int x = 0; x < kEpiPre; ++x) {
+    R.src[x] = ES_DIRECT;
+    R.sval[x] = 0.0;
+    R.fsub[x] = e ? e->fsub[x] : 0;
+    R.fleft[x] = e ? e->fleft[x] : 0;
+    R.ptr[x] = e ? e->ptr[x] : nullptr;
+    R.st0[x] = e ? (int)e->st0[x] : 0;
+    R.st1[x] = e ? (int)e->st1[x] : 0;
+    if (e && e->fast && x < e->next) {
+      if (R.st0[x] == 0 && R.st1[x] == 0) {
+        R.src[x] = ES_SCALAR;
+        R.sval[x] = R.ptr[x][0];
+      } else if (tile_free && R.tile < 0 && R.st0[x] != 0 && R.st1[x] != 0 && !__isShared(R.ptr[x])) {
+        R.src[x] = ES_TILE;
+        R.tile = x;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ double epi_operand(const EpiR& R, int x, const double* Es, int ers, int eks,
+                                              int m, int n, int mm, int nn) {
+  if (R.src[x] == ES_SCALAR) return R.sval[x];
+  if (R.src[x] == ES_TILE) return Es[mm * ers + nn * eks];
+  return R.ptr[x][(int64_t)m * R.st0[x] + (int64_t)n * R.st1[x]];
+}
+
+// the epilogue of output (m, n) (panel-local (mm, nn)) applied to dot value v
+template <int EK>
+__device__ __forceinline__ double epi_apply(const EpiR& R, const EpiDev* epi, const double* Es, int ers,
+                                            int eks, double v, int m, int n, int mm, int nn) {
+  if (EK == EK_NONE) return v;
+  if (EK == EK_CHAIN) {
+#pragma unroll
+    for (int x = 0; x < kEpiPre; ++x) {
+      if (x < R.nops) {
+        const double o = epi_operand(R, x, Es, ers, eks, m, n, mm, nn);
+        v = R.fleft[x] ? bin_f64(R.fsub[x], v, o) : bin_f64(R.fsub[x], o, v);
+      }
+    }
+    return v;
+  }
+  if (EK == EK_SELECT) {
+    const bool p = as_i64(epi_operand(R, 0, Es, ers, eks, m, n, mm, nn)) != 0;
+    const double o = epi_operand(R, 1, Es, ers, eks, m, n, mm, nn);
+    return R.fleft[0] ? (p ? v : o) : (p ? o : v);
+  }
+  double ev[kEpiPre];
+  epi_fetch(*epi, m, n, ev);
+  return epilogue_generic(*epi, ev, v, m, n);
+}
+
+struct DotArgs {
+  const double* A;
+  const double* B;
+  int sam, sak, sbk, sbn;
+  bool a_smem, b_smem;
+  double* out;
+  int som, son;
+  int M, K;
+};
+
+// Panel epilogue + store (all threads): the panel's raw dot values sit in
+// the C tile (row-major, stride kCS); thread t handles elements
+// e = t + kDotThreads*u of the 32 x 32 panel, (i, j) = (e >> 5, e & 31), so
+// consecutive threads store consecutive output columns.  EK is uniform.
+constexpr int kCS = 33;
+constexpr int kEmitPer = 1024 / kDotThreads;   // panel elements per thread
+
+template <int EK>
+__device__ __forceinline__ void dot_emit_panel(const double* Cs, const double* Es, const EpiR& Rs, int ers, int eks,
+                                            const EpiDev* epi, double* out, int som, int son, int m0, int n0,
+                                            int pm, int pn) {
+  double v[kEmitPer];
+  bool in[kEmitPer];
+#pragma unroll
+  for (int u = 0; u < kEmitPer; ++u) {
+    const int e = threadIdx.x + u * kDotThreads;
+    const int i = e >> 5, j = e & 31;
+    in[u] = i < pm && j < pn;
+    v[u] = in[u] ? Cs[i * kCS + j] : 0.0;
+  }
+  if (EK == EK_CHAIN || EK == EK_SELECT) {
+    const EpiR R = Rs;                 // registers; uniform decisions below
+    const int nx = EK == EK_SELECT ? 2 : R.nops;
+    double o[kEpiPre][kEmitPer];
+#pragma unroll
+    for (int x = 0; x < kEpiPre; ++x) {
+      if (x < nx) {
+        const int src = R.src[x];
+        if (src == ES_SCALAR) {
+#pragma unroll
+          for (int u = 0; u < kEmitPer; ++u) o[x][u] = R.sval[x];
+        } else if (src == ES_TILE) {
+#pragma unroll
+          for (int u = 0; u < kEmitPer; ++u) {
+            const int e = threadIdx.x + u * kDotThreads;
+            o[x][u] = in[u] ? Es[(e >> 5) * ers + (e & 31) * eks] : 0.0;
+          }
+        } else {
+          const double* pp = R.ptr[x] + (int64_t)m0 * R.st0[x] + (int64_t)n0 * R.st1[x];
+#pragma unroll
+          for (int u = 0; u < kEmitPer; ++u) {
+            const int e = threadIdx.x + u * kDotThreads;
+            o[x][u] = in[u] ? pp[(int64_t)(e >> 5) * R.st0[x] + (int64_t)(e & 31) * R.st1[x]] : 0.0;
+          }
+        }
+      }
+    }
+    if (EK == EK_SELECT) {
+#pragma unroll
+      for (int u = 0; u < kEmitPer; ++u) {
+        const bool p = as_i64(o[0][u]) != 0;
+        v[u] = R.fleft[0] ? (p ? v[u] : o[1][u]) : (p ? o[1][u] : v[u]);
+      }
+    } else {
+#pragma unroll
+      for (int x = 0; x < kEpiPre; ++x) {
+        if (x < nx) {
+          const bool left = R.fleft[x];
+#define GEVO_EMIT_OP(EXPR)                                                  \
+  _Pragma("unroll") for (int u = 0; u < kEmitPer; ++u) {                    \
+    const double a = left ? v[u] : o[x][u], b = left ? o[x][u] : v[u];     \
+    v[u] = (EXPR);                                                          \
+  }
+          switch (R.fsub[x]) {   // warp-uniform: one dispatch per micro-op
+            case GEVO_B_ADD: GEVO_EMIT_OP(__dadd_rn(a, b)); break;
+            case GEVO_B_SUB: GEVO_EMIT_OP(__dsub_rn(a, b)); break;
+            case GEVO_B_MUL: GEVO_EMIT_OP(__dmul_rn(a, b)); break;
+            case GEVO_B_DIV: GEVO_EMIT_OP(__ddiv_rn(a, b)); break;
+            default: GEVO_EMIT_OP(np_fmax(a, b)); break;
+          }
+#undef GEVO_EMIT_OP
+        }
+      }
+    }
+  } else if (EK == EK_GENERIC) {
+#pragma unroll
+    for (int u = 0; u < kEmitPer; ++u) {
+      if (in[u]) {
+        const int e = threadIdx.x + u * kDotThreads;
+        const int m = m0 + (e >> 5), n = n0 + (e & 31);
+        double ev[kEpiPre];
+        epi_fetch(*epi, m, n, ev);
+        v[u] = epilogue_generic(*epi, ev, v[u], m, n);
+      }
+    }
+  }
+  double* ob = out + (int64_t)m0 * som + (int64_t)n0 * son;
+#pragma unroll
+  for (int u = 0; u < kEmitPer; ++u) {
+    const int e = threadIdx.x + u * kDotThreads;
+    if (in[u]) ob[(int64_t)(e >> 5) * som + (int64_t)(e & 31) * son] = v[u];
+  }
+}
+
+template <int EK>
+__device__ __forceinline__ void dot_emit_dispatch(int ek, const double* Cs, const double* Es, const EpiR& R,
+                                                  int ers, int eks, const EpiDev* epi, double* out, int som,
+                                                  int son, int m0, int n0, int pm, int pn) {
+  switch (ek) {
+    case EK_NONE: dot_emit_panel<EK_NONE>(Cs, Es, R, ers, eks, epi, out, som, son, m0, n0, pm, pn); break;
+    case EK_CHAIN: dot_emit_panel<EK_CHAIN>(Cs, Es, R, ers, eks, epi, out, som, son, m0, n0, pm, pn); break;
+    case EK_SELECT: dot_emit_panel<EK_SELECT>(Cs, Es, R, ers, eks, epi, out, som, son, m0, n0, pm, pn); break;
+    default: dot_emit_panel<EK_GENERIC>(Cs, Es, R, ers, eks, epi, out, som, son, m0, n0, pm, pn); break;
+  }
+}
+
+// KIND: 0 FMA_CHAIN (DMMA; warp = 8 x 16 strip of a 32 x 32 panel), 1 ACC8
+// (DMMA; warp = one 8 x 8 tile x 8 chains; panels 32 x 16), 2 SEQ_NOFMA,
+// 3 integer (scalar; thread = 4 outputs of a 32 x 32 panel).  Output columns
+// [col0, col1).  After a panel's last chunk its values go to the C tile (the
+// slot's A region) and dot_emit_panel applies the epilogue and stores.
+template <int KIND>
+__device__ __forceinline__ void dot_pipeline(const DotArgs& dref, int col0, int col1, int mode, double* stage_buf,
+                                             const EpiDev* epi) {
+  static_assert(kDotWarps == 8, "dot tiling assumes 8 warps");
+  const DotArgs d = dref;   // registers: stores through d.out must not alias it
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  constexpr int PN = KIND == 1 ? 16 : kPanel;   // ACC8 panels are 32 x 16
+  constexpr bool perm = KIND == 1;
+  const int M = d.M, K = d.K;
+  const int ncols = col1 - col0;
+  const int npc = (ncols + PN - 1) / PN;
+  const int nch = (K + kKC - 1) / kKC;
+  const int total = ((M + kPanel - 1) / kPanel) * npc * nch;
+  const int ek = !epi ? EK_NONE : (epi->fast == 1 ? EK_CHAIN : (epi->fast == 2 ? EK_SELECT : EK_GENERIC));
+  // all of B in one persistent tile: staged once; each stage's second tile
+  // is then free for a full-matrix epilogue operand
+  const bool bpersist = nch == 1 && npc == 1;
+  // uniform per-instruction state in shared memory (registers go to the
+  // accumulators and the per-thread copy offsets)
+  __shared__ EpiR R;
+  __shared__ CopyPlan pa_, pb_, pe_;
+  if (threadIdx.x == 0) {
+    epi_init(R, ek == EK_CHAIN || ek == EK_SELECT ? epi : nullptr, bpersist);
+    plan_init(pa_, d.A, d.sam, d.sak, d.a_smem, perm);
+    plan_init(pb_, d.B, d.sbn, d.sbk, d.b_smem, perm);
+    if (R.tile >= 0) plan_init(pe_, R.ptr[R.tile], R.st0[R.tile], R.st1[R.tile], false, false);
+  }
+  __syncthreads();
+  const bool etile = R.tile >= 0;
+  const int oa = plan_o0(pa_), ob = plan_o0(pb_), oe = etile ? plan_o0(pe_) : 0;
+  const uint32_t ring = smem_u32(stage_buf);
+  double* Bp = stage_buf + kDotStages * 2 * kTileElems;
+
+  if (bpersist) stage(smem_u32(Bp), pb_, ob, col0, ncols, 0, K);
+  int lc = 0, lm0 = 0, ln0 = col0;     // load-side cursor: chunk, panel origin
+  auto load_next = [&](int slot) {
+    const uint32_t As = ring + 8u * (slot * 2 * kTileElems);
+    const uint32_t Xs = As + 8u * kTileElems;
+    const int k0 = lc * kKC;
+    const int nk = min(kKC, K - k0), pm = min(kPanel, M - lm0), pn = min(PN, col1 - ln0);
+    stage(As, pa_, oa, lm0, pm, k0, nk);
+    if (!bpersist) stage(Xs, pb_, ob, ln0, pn, k0, nk);
+    else if (etile) stage(Xs, pe_, oe, lm0, pm, ln0, pn);
+    if (++lc == nch) {
+      lc = 0;
+      ln0 += PN;
+      if (ln0 >= col1) { ln0 = col0; lm0 += kPanel; }
+    }
+  };
+#pragma unroll 1
+  for (int s = 0; s < kDotStages - 1; ++s) {
+    if (s < total) load_next(s);
+    cp_async_commit();
+  }
+
+  constexpr int NACC = KIND == 1 ? 16 : 4;
+  double acc[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+  const int rb = warp >> 1;
+  const int cb0 = KIND == 1 ? (warp & 1) : (warp & 1) * 2;
+  const int ars = cp_rs(pa_), aks = cp_ks(pa_), brs = cp_rs(pb_), bks = cp_ks(pb_);
+  const int lm = rb * 8 + g;          // lane's panel row (DMMA kinds)
+  const int ln = cb0 * 8 + 2 * t4;    // lane's first panel column
+  int c = 0, m0 = 0, n0 = col0;       // compute-side cursor
+  int slot = 0, lslot = kDotStages - 1;
+
+#pragma unroll 1
+  for (int s = 0; s < total; ++s) {
+    if (s + kDotStages - 1 < total) load_next(lslot);
+    cp_async_commit();
+    cp_async_wait<kDotStages - 1>();
+    __syncthreads();
+    const int k0 = c * kKC;
+    const int nk = min(kKC, K - k0);
+    const bool last = c == nch - 1;
+    double* As = stage_buf + slot * 2 * kTileElems;
+    // a persistent B tile holds every k (nch == 1); a streamed one this chunk's
+    const double* Bs = bpersist ? Bp : As + kTileElems;
+    const int pm = min(kPanel, M - m0), pn = min(PN, col1 - n0);
+    double* Cs = As;                    // C tile (after the A tile is consumed)
+
+    if (KIND == 0) {
+      const bool act0 = rb * 8 < pm && cb0 * 8 < pn;
+      const bool act1 = act0 && (cb0 + 1) * 8 < pn;
+      if (act0) {
+        const double* pa = As + lm * ars + t4 * aks;
+        const double* pb0 = Bs + (cb0 * 8 + g) * brs + t4 * bks;
+        const double* pb1 = pb0 + 8 * brs;
+        const int nq = nk >> 2;
+        const int qa = 4 * aks, qb = 4 * bks;
+        if (nq == 8 && act1) {
+          double fa[8], fb0[8], fb1[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            fa[q] = pa[q * qa];
+            fb0[q] = pb0[q * qb];
+            fb1[q] = pb1[q * qb];
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            dmma884(acc[0], acc[1], fa[q], fb0[q]);
+            dmma884(acc[2], acc[3], fa[q], fb1[q]);
+          }
+        } else {
+#pragma unroll 1
+          for (int q = 0; q < nq; ++q) {
+            const double a = pa[q * qa];
+            dmma884(acc[0], acc[1], a, pb0[q * qb]);
+            if (act1) dmma884(acc[2], acc[3], a, pb1[q * qb]);
+          }
+          // k tail (K % 4), last chunk only: scalar fma on this lane's outputs
+#pragma unroll 1
+          for (int kk = nq * 4; kk < nk; ++kk) {
+            const double a = As[lm * ars + kk * aks];
+            acc[0] = fma(a, Bs[ln * brs + kk * bks], acc[0]);
+            acc[1] = fma(a, Bs[(ln + 1) * brs + kk * bks], acc[1]);
+            if (act1) {
+              acc[2] = fma(a, Bs[(ln + 8) * brs + kk * bks], acc[2]);
+              acc[3] = fma(a, Bs[(ln + 9) * brs + kk * bks], acc[3]);
+            }
+          }
+        }
+      }
+      if (last) {
+        __syncthreads();                // every warp is done reading A
+        if (act0) {
+          Cs[lm * kCS + ln] = acc[0];
+          Cs[lm * kCS + ln + 1] = acc[1];
+          Cs[lm * kCS + ln + 8] = acc[2];
+          Cs[lm * kCS + ln + 9] = acc[3];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i] = 0.0;
+      }
+    } else if (KIND == 1) {
+      const int kmain = (mode == GEVO_D_ACC8_TAIL) ? (K & ~7) : K;
+      const bool act = rb * 8 < pm && cb0 * 8 < pn;
+      double r0 = 0.0, r1 = 0.0;
+      if (act) {
+        const double* pa = As + lm * ars + t4 * aks;
+        const double* pb = Bs + (cb0 * 8 + g) * brs + t4 * bks;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (k0 + j + 24 < kmain) {
+            // chain j's four k (j, j+8, j+16, j+24) sit at positions 4j..4j+3
+            dmma884(acc[2 * j], acc[2 * j + 1], pa[4 * j * aks], pb[4 * j * bks]);
+          } else {
+#pragma unroll 1
+            for (int t = 0; t < 4; ++t) {
+              const int kk = j + 8 * t;
+              if (k0 + kk >= kmain) break;
+              const int pk = 4 * j + t;
+              const double a = As[lm * ars + pk * aks];
+              acc[2 * j] = fma(a, Bs[ln * brs + pk * bks], acc[2 * j]);
+              acc[2 * j + 1] = fma(a, Bs[(ln + 1) * brs + pk * bks], acc[2 * j + 1]);
+            }
+          }
+        }
+        if (last) {
+          r0 = __dadd_rn(__dadd_rn(__dadd_rn(acc[0], acc[2]), __dadd_rn(acc[4], acc[6])),
+                         __dadd_rn(__dadd_rn(acc[8], acc[10]), __dadd_rn(acc[12], acc[14])));
+          r1 = __dadd_rn(__dadd_rn(__dadd_rn(acc[1], acc[3]), __dadd_rn(acc[5], acc[7])),
+                         __dadd_rn(__dadd_rn(acc[9], acc[11]), __dadd_rn(acc[13], acc[15])));
+#pragma unroll 1
+          for (int kk = kmain - k0; kk < nk; ++kk) {     // ACC8_TAIL: k >= K&~7
+            const int pk = ((kk & 7) << 2) | (kk >> 3);
+            const double a = As[lm * ars + pk * aks];
+            r0 = fma(a, Bs[ln * brs + pk * bks], r0);
+            r1 = fma(a, Bs[(ln + 1) * brs + pk * bks], r1);
+          }
+        }
+      }
+      if (last) {
+        __syncthreads();
+        if (act) {
+          Cs[lm * kCS + ln] = r0;
+          Cs[lm * kCS + ln + 1] = r1;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+      }
+    } else {
+      // scalar (KIND 2 f64 no-FMA, KIND 3 integer): thread owns outputs
+      // o = tid + kDotThreads u of the 32 x 32 panel
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int o = threadIdx.x + u * kDotThreads;
+        const int mm = o >> 5, nn = o & 31;
+        if (mm < pm && nn < pn) {
+          const double* pa = As + mm * ars;
+          const double* pb = Bs + nn * brs;
+          double v = acc[u];
+          if (KIND == 2) {
+#pragma unroll 1
+            for (int kk = 0; kk < nk; ++kk) v = __dadd_rn(v, __dmul_rn(pa[kk * aks], pb[kk * bks]));
+          } else {
+            uint64_t w = (uint64_t)as_i64(v);
+#pragma unroll 1
+            for (int kk = 0; kk < nk; ++kk)
+              w += (uint64_t)as_i64(pa[kk * aks]) * (uint64_t)as_i64(pb[kk * bks]);
+            v = as_w((int64_t)w);
+          }
+          acc[u] = v;
+        }
+      }
+      if (last) {
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int o = threadIdx.x + u * kDotThreads;
+          Cs[(o >> 5) * kCS + (o & 31)] = acc[u];
+          acc[u] = 0.0;
+        }
+      }
+    }
+    if (last) {
+      __syncthreads();                  // C tile complete
+      const int ers = etile ? cp_rs(pe_) : 0, eks = etile ? cp_ks(pe_) : 0;
+      dot_emit_dispatch<0>(ek, Cs, As + kTileElems, R, ers, eks, epi, d.out, d.som, d.son, m0, n0, pm, pn);
+    }
+    if (++c == nch) {
+      c = 0;
+      n0 += PN;
+      if (n0 >= col1) { n0 = col0; m0 += kPanel; }
+    }
+    slot = slot + 1 == kDotStages ? 0 : slot + 1;
+    lslot = lslot + 1 == kDotStages ? 0 : lslot + 1;
+    __syncthreads();   // buffer `slot` is refilled next iteration
+  }
+  cp_async_wait<0>();
+}
+
+template <int KIND>
+__device__ __noinline__ void dot_run(const DotArgs& d, int col0, int col1, int mode, double* stage_buf,
+                                     const EpiDev* epi) {
+  dot_pipeline<KIND>(d, col0, col1, mode, stage_buf, epi);
+}
+
+
+// ---------------------------------------------------------------------------
+// Fast paths for the two dot shapes that dominate the workloads (FMA chain,
+// every staged operand made of whole 16-byte-aligned lines):
+//   KSTREAM  one <= 32 x 32 output panel, K streamed in 32-k chunks
+//            (x . w1, K = 784: the forward pass)
+//   PANELS   K <= 32 and <= 32 columns: B staged once, the rows streamed in
+//            32-row panels, each with its full-matrix epilogue operand
+//            (x^T . delta fused with w1 - lr * (.): the weight update)
+// Each thread keeps running source pointers for its two 16-byte copies per
+// operand tile, so a stage costs a handful of instructions.
+struct VecCopy {
+  const double* p0;    // thread's copy 0 at the current stage
+  int64_t so;          // copy 1 = copy 0 + so
+  int64_t adv;         // advance per stage
+  uint32_t d0;         // smem byte offset of copy 0 within a tile
+  int line0, f;        // cross (line) index of copy 0, element index along the line
+  bool kmaj;           // lines run along k (rows of the tile are r)
+};
+
+__device__ __forceinline__ void vec_init(VecCopy& v, const double* p, int sr, int sk, int adv_elems) {
+  const int ar = sr < 0 ? -sr : sr, ak = sk < 0 ? -sk : sk;
+  v.kmaj = ak != 0 && (ar == 0 || ak <= ar);
+  const int cross = v.kmaj ? sr : sk;
+  const int t = threadIdx.x;
+  v.line0 = t >> 4;
+  v.f = (t & 15) * 2;
+  v.p0 = p + (int64_t)v.line0 * cross + v.f;
+  v.so = (int64_t)16 * cross;
+  v.adv = adv_elems;
+  v.d0 = 8u * (v.line0 * kTS + v.f);
+}
+
+__device__ __forceinline__ bool vec_ok(const double* p, int sr, int sk, int rext, int kext) {
+  const int ar = sr < 0 ? -sr : sr, ak = sk < 0 ? -sk : sk;
+  const bool kmaj = ak != 0 && (ar == 0 || ak <= ar);
+  const int cross = kmaj ? sr : sk, along = kmaj ? sk : sr;
+  return along == 1 && (cross & 1) == 0 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0) &&
+         ((kmaj ? kext : rext) & 1) == 0;
+}
+
+// issue one tile (nr x nk valid) of a VecCopy operand into smem tile `tile`
+__device__ __forceinline__ void vec_stage(const VecCopy& v, uint32_t tile, int nr, int nk) {
+  const int nline = v.kmaj ? nr : nk, nlen = v.kmaj ? nk : nr;
+  if (v.f >= nlen) return;
+  const int bytes = nlen - v.f >= 2 ? 16 : 8;
+  if (v.line0 < nline) cp_async16(tile + v.d0, v.p0, bytes);
+  if (v.line0 + 16 < nline) cp_async16(tile + v.d0 + 8u * 16 * kTS, v.p0 + v.so, bytes);
+}
+
+#ifdef GEVO_DOT_TIMING
+// diagnostics build only: per-phase cycles of dot_fast into profile slots of
+// the unused op class 0 (phase p -> slot 2p)
+__device__ unsigned long long* g_dot_prof;
+#define GEVO_TSTAMP(v) long long v = 0; if (threadIdx.x == 0) v = clock64();
+#define GEVO_TACC(p, a, b) if (threadIdx.x == 0 && g_dot_prof) { atomicAdd(g_dot_prof + 4 * (p), (unsigned long long)((b) - (a))); atomicAdd(g_dot_prof + 4 * (p) + 1, 1ULL); }
+#else
+#define GEVO_TSTAMP(v)
+#define GEVO_TACC(p, a, b)
+#endif
+
+template <bool PANELS>
+__device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, double* stage_buf,
+                                      const EpiDev* epi) {
+  const DotArgs d = dref;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int M = d.M, K = d.K, ncols = col1 - col0;
+  const int ek = !epi ? EK_NONE : (epi->fast == 1 ? EK_CHAIN : (epi->fast == 2 ? EK_SELECT : EK_GENERIC));
+  __shared__ EpiR R;
+  if (threadIdx.x == 0) epi_init(R, ek == EK_CHAIN || ek == EK_SELECT ? epi : nullptr, PANELS);
+  __syncthreads();
+  const bool etile = PANELS && R.tile >= 0;
+  const int total = PANELS ? (M + kPanel - 1) / kPanel : (K + kKC - 1) / kKC;
+  const uint32_t ring = smem_u32(stage_buf);
+  double* Bp = stage_buf + kDotStages * 2 * kTileElems;
+
+  VecCopy va, vx;        // A; second tile: B chunk (KSTREAM) or epilogue operand (PANELS)
+  int brs, bks;
+  if (PANELS) {
+    vec_init(va, d.A + (int64_t)col0 * 0, d.sam, d.sak, 32 * d.sam);
+    if (etile) vec_init(vx, R.ptr[R.tile] + (int64_t)col0 * R.st1[R.tile], R.st0[R.tile], R.st1[R.tile],
+                        32 * R.st0[R.tile]);
+    // B (K x ncols) once, any layout
+    CopyPlan pb;
+    plan_init(pb, d.B + (int64_t)col0 * d.sbn, d.sbn, d.sbk, d.b_smem, false);
+    stage(smem_u32(Bp), pb, plan_o0(pb), 0, ncols, 0, K);
+    brs = cp_rs(pb);
+    bks = cp_ks(pb);
+  } else {
+    vec_init(va, d.A, d.sam, d.sak, 32 * d.sak);
+    vec_init(vx, d.B + (int64_t)col0 * d.sbn, d.sbn, d.sbk, 32 * d.sbk);
+    brs = vx.kmaj ? kTS : 1;
+    bks = vx.kmaj ? 1 : kTS;
+  }
+  const int ars = va.kmaj ? kTS : 1, aks = va.kmaj ? 1 : kTS;
+  const int ers = vx.kmaj ? kTS : 1, eks = vx.kmaj ? 1 : kTS;
+
+  // stage i covers rows [32i, ..) (PANELS) or k [32i, ..) (KSTREAM)
+  auto load = [&](int i, int slot) {
+    const uint32_t As = ring + 8u * (slot * 2 * kTileElems);
+    if (PANELS) {
+      const int pm = min(kPanel, M - i * kPanel);
+      vec_stage(va, As, pm, K);
+      if (etile) vec_stage(vx, As + 8u * kTileElems, pm, ncols);
+    } else {
+      const int nk = min(kKC, K - i * kKC);
+      vec_stage(va, As, M, nk);
+      vec_stage(vx, As + 8u * kTileElems, ncols, nk);
+    }
+    va.p0 += va.adv;
+    vx.p0 += vx.adv;
+  };
+#pragma unroll 1
+  for (int i = 0; i < kDotStages - 1; ++i) {
+    if (i < total) load(i, i);
+    cp_async_commit();
+  }
+  const int rb = warp >> 1, cb0 = (warp & 1) * 2;
+  const int lm = rb * 8 + g, ln = cb0 * 8 + 2 * t4;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  int slot = 0, lslot = kDotStages - 1;
+#pragma unroll 1
+  for (int s = 0; s < total; ++s) {
+    GEVO_TSTAMP(ta)
+    if (s + kDotStages - 1 < total) load(s + kDotStages - 1, lslot);
+    cp_async_commit();
+    GEVO_TSTAMP(tl)
+    cp_async_wait<kDotStages - 1>();
+    __syncthreads();
+    GEVO_TSTAMP(tb)
+    GEVO_TACC(1, ta, tl)
+    GEVO_TACC(2, tl, tb)
+    double* As = stage_buf + slot * 2 * kTileElems;
+    const double* Bs = PANELS ? Bp : As + kTileElems;
+    const int pm = PANELS ? min(kPanel, M - s * kPanel) : M;
+    const int nk = PANELS ? K : min(kKC, K - s * kKC);
+    const bool last = PANELS || s == total - 1;
+    const bool act0 = rb * 8 < pm && cb0 * 8 < ncols;
+    const bool act1 = act0 && (cb0 + 1) * 8 < ncols;
+    if (act0) {
+      const double* pa = As + lm * ars + t4 * aks;
+      const double* pb0 = Bs + (cb0 * 8 + g) * brs + t4 * bks;
+      const double* pb1 = pb0 + 8 * brs;
+      const int nq = nk >> 2;
+      const int qa = 4 * aks, qb = 4 * bks;
+      if (nq == 8 && act1) {
+        // all 24 fragments first (one LDS latency), then 16 back-to-back DMMAs
+        double fa[8], fb0[8], fb1[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          fa[q] = pa[q * qa];
+          fb0[q] = pb0[q * qb];
+          fb1[q] = pb1[q * qb];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          dmma884(acc[0], acc[1], fa[q], fb0[q]);
+          dmma884(acc[2], acc[3], fa[q], fb1[q]);
+        }
+      } else {
+#pragma unroll 1
+        for (int q = 0; q < nq; ++q) {
+          const double a = pa[q * qa];
+          dmma884(acc[0], acc[1], a, pb0[q * qb]);
+          if (act1) dmma884(acc[2], acc[3], a, pb1[q * qb]);
+        }
+#pragma unroll 1
+        for (int kk = nq * 4; kk < nk; ++kk) {
+          const double a = As[lm * ars + kk * aks];
+          acc[0] = fma(a, Bs[ln * brs + kk * bks], acc[0]);
+          acc[1] = fma(a, Bs[(ln + 1) * brs + kk * bks], acc[1]);
+          if (act1) {
+            acc[2] = fma(a, Bs[(ln + 8) * brs + kk * bks], acc[2]);
+            acc[3] = fma(a, Bs[(ln + 9) * brs + kk * bks], acc[3]);
+          }
+        }
+      }
+    }
+    GEVO_TSTAMP(tc)
+    GEVO_TACC(3, tb, tc)
+    if (last) {
+      __syncthreads();                // A consumed: its region becomes the C tile
+      double* Cs = As;
+      if (act0) {
+        Cs[lm * kCS + ln] = acc[0];
+        Cs[lm * kCS + ln + 1] = acc[1];
+        Cs[lm * kCS + ln + 8] = acc[2];
+        Cs[lm * kCS + ln + 9] = acc[3];
+      }
+      acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+      __syncthreads();
+      const int m0 = PANELS ? s * kPanel : 0;
+      GEVO_TSTAMP(te0)
+      GEVO_TACC(4, tc, te0)
+      dot_emit_dispatch<0>(ek, Cs, As + kTileElems, R, ers, eks, epi, d.out, d.som, d.son, m0, col0, pm, ncols);
+      GEVO_TSTAMP(te1)
+      GEVO_TACC(5, te0, te1)
+    }
+    slot = slot + 1 == kDotStages ? 0 : slot + 1;
+    lslot = lslot + 1 == kDotStages ? 0 : lslot + 1;
+    GEVO_TSTAMP(tf0)
+    __syncthreads();
+    GEVO_TSTAMP(tf1)
+    GEVO_TACC(6, tf0, tf1)
+  }
+  cp_async_wait<0>();
+}
+
+// PANELS needs its tile-staged epilogue operand (the first full-matrix one,
+// see epi_init) to be made of whole aligned lines
+__device__ __forceinline__ bool dot_etile_ok(const EpiDev* e, int ncols, int M) {
+  for (int x = 0; x < kEpiPre && x < e->next; ++x) {
+    if ((e->st0[x] == 0 && e->st1[x] == 0) || e->st0[x] == 0 || e->st1[x] == 0 || __isShared(e->ptr[x])) continue;
+    return vec_ok(e->ptr[x], (int)e->st0[x], (int)e->st1[x], M, ncols);
+  }
+  return true;
+}
+
+// columns [col0, col1) of a DOT in summation order `mode`
+__device__ __forceinline__ void dot_columns(const DotArgs& d, int col0, int col1, int mode, bool integer,
+                                            double* stage_buf, const EpiDev* epi) {
+  if (col0 >= col1) return;
+  if (integer) dot_run<3>(d, col0, col1, mode, stage_buf, epi);
+  else if (mode == GEVO_D_SEQ_NOFMA) dot_run<2>(d, col0, col1, mode, stage_buf, epi);
+  else if (mode == GEVO_D_FMA_CHAIN) {
+    const int ncols = col1 - col0;
+    const bool a_ok = !d.a_smem && vec_ok(d.A, d.sam, d.sak, d.M, d.K);
+    if (ncols <= kPanel && d.M <= kPanel && d.K > kKC && a_ok && !d.b_smem &&
+        vec_ok(d.B + (int64_t)col0 * d.sbn, d.sbn, d.sbk, ncols, d.K)) {
+      dot_fast<false>(d, col0, col1, stage_buf, epi);
+    } else if (ncols <= kPanel && d.K <= kKC && a_ok && (!epi || epi->fast == 0 || dot_etile_ok(epi, ncols, d.M))) {
+      dot_fast<true>(d, col0, col1, stage_buf, epi);
+    } else {
+      dot_run<0>(d, col0, col1, mode, stage_buf, epi);
+    }
+  }
+  else dot_run<1>(d, col0, col1, mode, stage_buf, epi);
+}
+
+}  // namespace gevo

@@ -18,11 +18,11 @@
 
 namespace gevo {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;   // 8 warps; 2 CTAs/SM (128 registers)
 #ifndef GEVO_MIN_BLOCKS
 #define GEVO_MIN_BLOCKS 2   // CTAs per SM the register budget is sized for
 #endif
-constexpr int kInstrCache = 80;   // instructions staged in shared memory
+constexpr int kInstrCache = 64;   // instructions staged in shared memory
 
 // a dot's fused elementwise epilogue, decoded once per instruction into
 // shared memory (gevo_plan.h, "Dot epilogues")
@@ -60,15 +60,16 @@ __device__ __forceinline__ double* opptr(const Shared& S, const gevo_operand& o)
 // thread keeps kEwUnroll independent elements in flight for memory-level
 // parallelism.
 // ---------------------------------------------------------------------------
-constexpr int kEwUnroll = 4;
+constexpr int kEwUnroll = 8;
 
 struct EwDesc {
   double* out;
   const double* in[3];
-  int64_t off[4];      // out, in0, in1, in2
-  int32_t step[4];     // linear: 1, scalar: 0 (fast path)
-  int n, rank, kin, kout, sub;
-  bool strided;
+  int off[4];          // out, in0, in1, in2 (element offsets)
+  int step[4];         // linear mode: 1 (C order) or 0 (scalar)
+  int sr[4], sc[4];    // 2-D mode: row / column strides
+  int n, rank, C;
+  int mode;            // 0 linear, 1 2-D (rank <= 2), 2 generic unravel
 };
 
 struct FAdd { __device__ double operator()(double a, double b, double) const { return __dadd_rn(a, b); } };
@@ -90,49 +91,69 @@ struct FUnGeneric {
   __device__ double operator()(double a, double, double) const { return apply_unary(sub, kin, kout, a); }
 };
 
+// every operand C-ordered like the output (or a scalar): address = off + i*step
 template <int NIN, class F>
-__device__ __noinline__ void ew_linear(const EwDesc d, F f) {
-  const int bd = blockDim.x;
-  for (int base = threadIdx.x; base < d.n; base += kEwUnroll * bd) {
+__device__ __forceinline__ void ew_linear(const EwDesc& d, F f) {
+  for (int base = threadIdx.x; base < d.n; base += kEwUnroll * kThreads) {
     double a[kEwUnroll], b[kEwUnroll], c[kEwUnroll];
 #pragma unroll
     for (int u = 0; u < kEwUnroll; ++u) {
-      const int i = base + u * bd;
+      const int i = base + u * kThreads;
       if (i < d.n) {
-        a[u] = d.in[0][d.off[1] + (int64_t)i * d.step[1]];
-        if (NIN > 1) b[u] = d.in[1][d.off[2] + (int64_t)i * d.step[2]];
-        if (NIN > 2) c[u] = d.in[2][d.off[3] + (int64_t)i * d.step[3]];
+        a[u] = d.in[0][d.off[1] + i * d.step[1]];
+        if (NIN > 1) b[u] = d.in[1][d.off[2] + i * d.step[2]];
+        if (NIN > 2) c[u] = d.in[2][d.off[3] + i * d.step[3]];
       }
     }
 #pragma unroll
     for (int u = 0; u < kEwUnroll; ++u) {
-      const int i = base + u * bd;
-      if (i < d.n) d.out[d.off[0] + (int64_t)i * d.step[0]] = f(a[u], NIN > 1 ? b[u] : 0.0, NIN > 2 ? c[u] : 0.0);
+      const int i = base + u * kThreads;
+      if (i < d.n) d.out[d.off[0] + i * d.step[0]] = f(a[u], NIN > 1 ? b[u] : 0.0, NIN > 2 ? c[u] : 0.0);
     }
   }
 }
 
+// rank <= 2, any strides: element i = (r, c) walked incrementally (no
+// division per element)
 template <int NIN, class F>
-__device__ __noinline__ void ew_strided(const gevo_instr& I, const EwDesc d, F f) {
-  int32_t shp[GEVO_MAXR], st[4][GEVO_MAXR];
-  const gevo_operand* ops[4] = {&I.out, &I.in[0], &I.in[1], &I.in[2]};
+__device__ __forceinline__ void ew_2d(const EwDesc& d, F f) {
+  const int C = d.C;
+  const int q = kThreads / C, rm = kThreads - q * C;
+  int r = threadIdx.x / C, c = threadIdx.x - (threadIdx.x / C) * C;
+  for (int base = threadIdx.x; base < d.n; base += kEwUnroll * kThreads) {
+    double a[kEwUnroll], b[kEwUnroll], x[kEwUnroll];
+    int ao[kEwUnroll];
 #pragma unroll
-  for (int r = 0; r < GEVO_MAXR; ++r) {
-    shp[r] = I.shp[r];
+    for (int u = 0; u < kEwUnroll; ++u) {
+      if (base + u * kThreads < d.n) {
+        ao[u] = d.off[0] + r * d.sr[0] + c * d.sc[0];
+        a[u] = d.in[0][d.off[1] + r * d.sr[1] + c * d.sc[1]];
+        if (NIN > 1) b[u] = d.in[1][d.off[2] + r * d.sr[2] + c * d.sc[2]];
+        if (NIN > 2) x[u] = d.in[2][d.off[3] + r * d.sr[3] + c * d.sc[3]];
+      }
+      c += rm;
+      r += q;
+      if (c >= C) { c -= C; ++r; }
+    }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) st[k][r] = (k <= NIN) ? ops[k]->st[r] : 0;
+    for (int u = 0; u < kEwUnroll; ++u)
+      if (base + u * kThreads < d.n) d.out[ao[u]] = f(a[u], NIN > 1 ? b[u] : 0.0, NIN > 2 ? x[u] : 0.0);
   }
+}
+
+template <int NIN, class F>
+__device__ __forceinline__ void ew_unravel(const gevo_instr& I, const EwDesc& d, F f) {
+  const gevo_operand* ops[4] = {&I.out, &I.in[0], &I.in[1], &I.in[2]};
   const int rank = d.rank;
-  for (int i = threadIdx.x; i < d.n; i += blockDim.x) {
+  for (int i = threadIdx.x; i < d.n; i += kThreads) {
     int idx[GEVO_MAXR];
-    unravel(i, rank, shp, idx);
+    unravel(i, rank, I.shp, idx);
     int64_t ad[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       int64_t v = d.off[k];
-#pragma unroll
-      for (int r = 0; r < GEVO_MAXR; ++r)
-        if (r < rank) v += (int64_t)idx[r] * st[k][r];
+      if (k <= NIN)
+        for (int r = 0; r < rank; ++r) v += (int64_t)idx[r] * ops[k]->st[r];
       ad[k] = v;
     }
     const double a = d.in[0][ad[1]];
@@ -142,10 +163,14 @@ __device__ __noinline__ void ew_strided(const gevo_instr& I, const EwDesc d, F f
   }
 }
 
+// (d is copied into registers: through the reference, every store to d.out
+// could alias the caller's descriptor and would force a reload)
 template <int NIN, class F>
-__device__ __forceinline__ void ew_run(const gevo_instr& I, const EwDesc& d, F f) {
-  if (d.strided) ew_strided<NIN>(I, d, f);
-  else ew_linear<NIN>(d, f);
+__device__ __noinline__ void ew_run(const gevo_instr& I, const EwDesc& dref, F f) {
+  const EwDesc d = dref;
+  if (d.mode == 0) ew_linear<NIN>(d, f);
+  else if (d.mode == 1) ew_2d<NIN>(d, f);
+  else ew_unravel<NIN>(I, d, f);
 }
 
 __device__ __noinline__ void run_elementwise(const Shared& S, const gevo_instr& I) {
@@ -153,36 +178,42 @@ __device__ __noinline__ void run_elementwise(const Shared& S, const gevo_instr& 
   const int op = I.op;
   d.n = I.n;
   d.rank = I.rank;
-  d.kin = I.kin;
-  d.kout = I.kout;
-  d.sub = I.sub;
   d.out = opptr(S, I.out);
   d.off[0] = I.out.off;
   const int nin = op == GEVO_OP_UNARY ? 1 : (op == GEVO_OP_BINARY ? 2 : 3);
-  d.strided = I.aux2[0] == AM_STRIDED;
+  bool strided = I.aux2[0] == AM_STRIDED;
   d.step[0] = I.aux2[0] == AM_LINEAR ? 1 : 0;
+  const gevo_operand* ops[4] = {&I.out, &I.in[0], &I.in[1], &I.in[2]};
   for (int k = 0; k < 3; ++k) {
     if (k < nin) {
       d.in[k] = opptr(S, I.in[k]);
       d.off[k + 1] = I.in[k].off;
       d.step[k + 1] = I.aux2[k + 1] == AM_LINEAR ? 1 : 0;
-      d.strided |= I.aux2[k + 1] == AM_STRIDED;
+      strided |= I.aux2[k + 1] == AM_STRIDED;
     } else {
       d.in[k] = d.in[0];
       d.off[k + 1] = 0;
       d.step[k + 1] = 0;
     }
   }
+  d.mode = !strided ? 0 : (d.rank <= 2 ? 1 : 2);
+  d.C = d.rank == 2 ? I.shp[1] : (d.rank == 1 ? I.shp[0] : 1);
+  for (int k = 0; k < 4; ++k) {
+    const bool used = k <= nin;
+    d.sr[k] = used && d.rank == 2 ? ops[k]->st[0] : 0;
+    d.sc[k] = used && d.rank >= 1 ? ops[k]->st[d.rank - 1] : 0;
+  }
+  const int kin = I.kin, sub = I.sub;
   if (op == GEVO_OP_SELECT) { ew_run<3>(I, d, FSel()); return; }
   if (op == GEVO_OP_UNARY) {
-    if (d.sub == GEVO_U_COPY) { ew_run<1>(I, d, FCopy()); return; }
-    if (d.kin == GEVO_K_F64 && d.sub == GEVO_U_EXP) { ew_run<1>(I, d, FExp()); return; }
-    if (d.kin == GEVO_K_F64 && d.sub == GEVO_U_NEG) { ew_run<1>(I, d, FNeg()); return; }
-    ew_run<1>(I, d, FUnGeneric{d.sub, d.kin, d.kout});
+    if (sub == GEVO_U_COPY) { ew_run<1>(I, d, FCopy()); return; }
+    if (kin == GEVO_K_F64 && sub == GEVO_U_EXP) { ew_run<1>(I, d, FExp()); return; }
+    if (kin == GEVO_K_F64 && sub == GEVO_U_NEG) { ew_run<1>(I, d, FNeg()); return; }
+    ew_run<1>(I, d, FUnGeneric{sub, kin, I.kout});
     return;
   }
-  if (d.kin == GEVO_K_F64) {
-    switch (d.sub) {
+  if (kin == GEVO_K_F64) {
+    switch (sub) {
       case GEVO_B_ADD: ew_run<2>(I, d, FAdd()); return;
       case GEVO_B_SUB: ew_run<2>(I, d, FSub()); return;
       case GEVO_B_MUL: ew_run<2>(I, d, FMul()); return;
@@ -191,14 +222,34 @@ __device__ __noinline__ void run_elementwise(const Shared& S, const gevo_instr& 
       case GEVO_B_GT: ew_run<2>(I, d, FGt()); return;
     }
   }
-  ew_run<2>(I, d, FBinGeneric{d.sub, d.kin});
+  ew_run<2>(I, d, FBinGeneric{sub, kin});
 }
 
 __device__ __noinline__ void run_pad(const Shared& S, const gevo_instr& I) {
   double* out = opptr(S, I.out);
   const double* in = opptr(S, I.in[0]);
   const double pv = opptr(S, I.in[1])[I.in[1].off];
-  for (int i = threadIdx.x; i < I.n; i += blockDim.x) {
+  if (I.rank <= 2) {
+    // (r, c) walked incrementally; rank 1 is one row
+    const bool two = I.rank == 2;
+    const int C = two ? I.shp[1] : (I.rank == 1 ? I.shp[0] : 1);
+    const int lo0 = two ? I.aux[0] : 0, lo1 = I.rank >= 1 ? I.aux[I.rank - 1] : 0;
+    const int ex0 = two ? I.aux2[0] : 1, ex1 = I.rank >= 1 ? I.aux2[I.rank - 1] : 1;
+    const int is0 = two ? I.in[0].st[0] : 0, is1 = I.rank >= 1 ? I.in[0].st[I.rank - 1] : 0;
+    const int os0 = two ? I.out.st[0] : 0, os1 = I.rank >= 1 ? I.out.st[I.rank - 1] : 0;
+    const int q = kThreads / C, rm = kThreads - q * C;
+    int r = threadIdx.x / C, c = threadIdx.x - (threadIdx.x / C) * C;
+    for (int i = threadIdx.x; i < I.n; i += kThreads) {
+      const int j0 = r - lo0, j1 = c - lo1;
+      const bool inside = j0 >= 0 && j0 < ex0 && j1 >= 0 && j1 < ex1;
+      out[I.out.off + r * os0 + c * os1] = inside ? in[I.in[0].off + j0 * is0 + j1 * is1] : pv;
+      c += rm;
+      r += q;
+      if (c >= C) { c -= C; ++r; }
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < I.n; i += kThreads) {
     int idx[GEVO_MAXR];
     unravel(i, I.rank, I.shp, idx);
     bool inside = true;
@@ -251,41 +302,7 @@ __device__ __noinline__ void run_reduce(const Shared& S, const gevo_instr& I) {
   }
 }
 
-__device__ __forceinline__ double dot_elem(int mode, const double* a, int64_t sa,
-                                           const double* b, int64_t sb, int K) {
-  if (mode == GEVO_D_FMA_CHAIN) {
-    double acc = 0.0;
-    for (int k = 0; k < K; ++k) acc = fma(a[k * sa], b[k * sb], acc);
-    return acc;
-  }
-  if (mode == GEVO_D_SEQ_NOFMA) {
-    double acc = 0.0;
-    for (int k = 0; k < K; ++k) acc = __dadd_rn(acc, __dmul_rn(a[k * sa], b[k * sb]));
-    return acc;
-  }
-  // 8 lane accumulators over k, then the pairwise lane tree
-  double l[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) l[j] = 0.0;
-  int kmain = (mode == GEVO_D_ACC8_TAIL) ? (K & ~7) : K;
-  for (int k = 0; k < kmain; ++k) l[k & 7] = fma(a[k * sa], b[k * sb], l[k & 7]);
-  double r = __dadd_rn(__dadd_rn(__dadd_rn(l[0], l[1]), __dadd_rn(l[2], l[3])),
-                       __dadd_rn(__dadd_rn(l[4], l[5]), __dadd_rn(l[6], l[7])));
-  for (int k = kmain; k < K; ++k) r = fma(a[k * sa], b[k * sb], r);
-  return r;
-}
-
-// D(8x8) += A(8x4) B(4x8) on the FP64 tensor path.  Probed on B200:
-// bit-identical to four chained fma() in k order (tests/tools/dmma_probe.cu),
-// so an 8x8 tile accumulated over k0 = 0, 4, 8, ... reproduces the
-// reference's single-accumulator FMA chain (OpenBLAS dgemm kernels) exactly.
-__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
-}
-
-// FMA-chain dots (see dot_direct below) and fused epilogues.
-constexpr int kStageElems = 0;   // no staging region (direct-load dots)
+// fused dot epilogues (the DOT itself: dot_staged.cuh)
 
 // decode the EXT records following a DOT (thread 0; caller syncs)
 __device__ void decode_epilogue(Shared& S, const gevo_instr* ext, int n_ext, int nops) {
@@ -413,232 +430,9 @@ __device__ __forceinline__ double epilogue(const EpiDev& e, const double* ev, do
   return epilogue_generic(e, ev, v, r, c);
 }
 
-// Barrier-free FMA-chain dot: every warp streams its own DMMA fragments
-// straight from memory (L1/L2; shared memory for the smem arena), eight
-// k-steps (32 k) per group, with the next group's loads issued before the
-// current group's DMMAs (register double buffer).  Warp strips are 8 rows x
-// 16 columns (two 8x8 tiles sharing the A fragment); strips are dealt to
-// warps round-robin.  Out-of-range rows/columns read a clamped (valid)
-// address and are simply not stored.  Each output element is one fma chain
-// over k = 0..K-1 in order, so the result is the reference's bit for bit.
-constexpr int kGrp = 4;   // k-steps (of 4) per software-pipeline group (long K)
-constexpr int kShortK = 8; // k-steps held in registers by the short-K variant
-
-struct DotGeom {
-  const double* A;
-  const double* B;
-  double* out;
-  int64_t sam, sak, sbk, sbn, som, son;
-  int M, K, ncols;
-};
-
-template <int EK>
-__device__ __forceinline__ void dot_store4(const DotGeom& d, const EpiDev* epi, int orow,
-                                           int cA, int cB, double c00, double c01, double c10,
-                                           double c11, const double (*ev)[kEpiPre]) {
-  if (orow >= d.M) return;
-  double* o = d.out + orow * d.som;
-  if (EK != EK_NONE) {
-    c00 = epilogue_k<EK>(*epi, ev[0], c00, orow, cA);
-    c01 = epilogue_k<EK>(*epi, ev[1], c01, orow, cA + 1);
-    c10 = epilogue_k<EK>(*epi, ev[2], c10, orow, cB);
-    c11 = epilogue_k<EK>(*epi, ev[3], c11, orow, cB + 1);
-  }
-  if (cA < d.ncols) o[cA * d.son] = c00;
-  if (cA + 1 < d.ncols) o[(cA + 1) * d.son] = c01;
-  if (cB < d.ncols) o[cB * d.son] = c10;
-  if (cB + 1 < d.ncols) o[(cB + 1) * d.son] = c11;
-}
-
-template <int EK>
-__device__ __forceinline__ void epi_fetch4(const DotGeom& d, const EpiDev* epi, int orow, int cA,
-                                           int cB, double (*ev)[kEpiPre]) {
-  if (EK == EK_NONE || orow >= d.M) return;
-  if (cA < d.ncols) epi_fetch(*epi, orow, cA, ev[0]);
-  if (cA + 1 < d.ncols) epi_fetch(*epi, orow, cA + 1, ev[1]);
-  if (cB < d.ncols) epi_fetch(*epi, orow, cB, ev[2]);
-  if (cB + 1 < d.ncols) epi_fetch(*epi, orow, cB + 1, ev[3]);
-}
-
-// k tail (K % 4 remaining k) for one lane's four accumulators, in chain order
-__device__ __forceinline__ void dot_ktail(const DotGeom& d, int orow, int cA, int cB,
-                                          double& c00, double& c01, double& c10, double& c11) {
-  const int K4 = d.K & ~3;
-  if (K4 == d.K || orow >= d.M) return;
-  const double* ar = d.A + orow * d.sam;
-  for (int k = K4; k < d.K; ++k) {
-    const double a = ar[k * d.sak];
-    const double* bk = d.B + k * d.sbk;
-    if (cA < d.ncols) c00 = fma(a, bk[cA * d.sbn], c00);
-    if (cA + 1 < d.ncols) c01 = fma(a, bk[(cA + 1) * d.sbn], c01);
-    if (cB < d.ncols) c10 = fma(a, bk[cB * d.sbn], c10);
-    if (cB + 1 < d.ncols) c11 = fma(a, bk[(cB + 1) * d.sbn], c11);
-  }
-}
-
-// Long K: each warp owns strips (8 rows x 16 cols) and streams K with a
-// register double buffer of kGrp k-steps.
-template <int EK>
-__device__ __noinline__ void dot_long_k(const DotGeom d, const EpiDev* epi) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int tm = (d.M + 7) >> 3, tn = (d.ncols + 15) >> 4;
-  const int nsteps = d.K >> 2;
-  const int ngrp = nsteps / kGrp, rem = nsteps - ngrp * kGrp;
-  const int64_t ska = 4 * d.sak, skb = 4 * d.sbk;
-  for (int strip = warp; strip < tm * tn; strip += nwarp) {
-    const int ti = strip / tn, tj = strip - ti * tn;
-    const int orow = ti * 8 + g, j0 = tj * 16 + g;
-    const int cA = tj * 16 + 2 * t4, cB = cA + 8;
-    const double* pa = d.A + min(orow, d.M - 1) * d.sam + t4 * d.sak;
-    const double* pb0 = d.B + min(j0, d.ncols - 1) * d.sbn + t4 * d.sbk;
-    const double* pb1 = d.B + min(j0 + 8, d.ncols - 1) * d.sbn + t4 * d.sbk;
-    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
-    // ping-pong register sets: the loads of group g+1 are in flight while
-    // the DMMAs of group g run; no register copies between groups (macros,
-    // not lambdas: every fragment index stays a compile-time constant)
-    double xa[kGrp], xb0[kGrp], xb1[kGrp], ya[kGrp], yb0[kGrp], yb1[kGrp];
-#define GEVO_LOAD(A_, B0_, B1_)                  \
-    {                                            \
-      _Pragma("unroll") for (int u = 0; u < kGrp; ++u) { \
-        A_[u] = pa[u * ska];                     \
-        B0_[u] = pb0[u * skb];                   \
-        B1_[u] = pb1[u * skb];                   \
-      }                                          \
-      pa += kGrp * ska;                          \
-      pb0 += kGrp * skb;                         \
-      pb1 += kGrp * skb;                         \
-    }
-#define GEVO_MMA(A_, B0_, B1_)                   \
-    {                                            \
-      _Pragma("unroll") for (int u = 0; u < kGrp; ++u) { \
-        dmma884(c00, c01, A_[u], B0_[u]);        \
-        dmma884(c10, c11, A_[u], B1_[u]);        \
-      }                                          \
-    }
-    if (ngrp > 0) GEVO_LOAD(xa, xb0, xb1);
-    int gi = 0;
-    for (; gi + 2 <= ngrp; gi += 2) {
-      GEVO_LOAD(ya, yb0, yb1);                   // group gi+1 in flight
-      GEVO_MMA(xa, xb0, xb1);                    // group gi
-      if (gi + 2 < ngrp) GEVO_LOAD(xa, xb0, xb1);  // group gi+2 in flight
-      GEVO_MMA(ya, yb0, yb1);                    // group gi+1
-    }
-    if (gi < ngrp) GEVO_MMA(xa, xb0, xb1);       // odd last group
-#undef GEVO_LOAD
-#undef GEVO_MMA
-    for (int u = 0; u < rem; ++u) {
-      dmma884(c00, c01, pa[0], pb0[0]);
-      dmma884(c10, c11, pa[0], pb1[0]);
-      pa += ska;
-      pb0 += skb;
-      pb1 += skb;
-    }
-    dot_ktail(d, orow, cA, cB, c00, c01, c10, c11);
-    double ev[4][kEpiPre];
-    epi_fetch4<EK>(d, epi, orow, cA, cB, ev);
-    dot_store4<EK>(d, epi, orow, cA, cB, c00, c01, c10, c11, ev);
-  }
-}
-
-// Short K (K <= 4*kShortK): warp w keeps one column strip (tj = w % tn) and
-// its B fragments in registers for every row strip it visits; the next row
-// strip's A fragments and epilogue operands are fetched while the current
-// one's DMMAs run.
-template <int EK>
-__device__ __noinline__ void dot_short_k(const DotGeom d, const EpiDev* epi) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int tm = (d.M + 7) >> 3, tn = (d.ncols + 15) >> 4;
-  const int nsteps = d.K >> 2;
-  const int64_t ska = 4 * d.sak, skb = 4 * d.sbk;
-  const int wpc = nwarp / tn;                // warps per column strip (>= 1)
-  const int tj = warp % tn, w0 = warp / tn;
-  if (w0 >= wpc) return;
-  const int j0 = tj * 16 + g;
-  const int cA = tj * 16 + 2 * t4, cB = cA + 8;
-  double fb0[kShortK], fb1[kShortK];
-  {
-    const double* pb0 = d.B + min(j0, d.ncols - 1) * d.sbn + t4 * d.sbk;
-    const double* pb1 = d.B + min(j0 + 8, d.ncols - 1) * d.sbn + t4 * d.sbk;
-#pragma unroll
-    for (int u = 0; u < kShortK; ++u) {
-      fb0[u] = u < nsteps ? pb0[u * skb] : 0.0;
-      fb1[u] = u < nsteps ? pb1[u * skb] : 0.0;
-    }
-  }
-  if (w0 >= tm) return;
-  // ping-pong register sets X / Y: the next row strip's A fragments and
-  // epilogue operands load while the current strip's DMMAs and stores run
-  double xa[kShortK], ya[kShortK];
-  double xev[4][kEpiPre], yev[4][kEpiPre];
-#define GEVO_FETCH(TI, FA, EV)                                          \
-  {                                                                      \
-    const int orow_ = (TI) * 8 + g;                                      \
-    const double* pa_ = d.A + min(orow_, d.M - 1) * d.sam + t4 * d.sak;  \
-    _Pragma("unroll") for (int u = 0; u < kShortK; ++u)                  \
-      FA[u] = u < nsteps ? pa_[u * ska] : 0.0;                           \
-    epi_fetch4<EK>(d, epi, orow_, cA, cB, EV);                           \
-  }
-#define GEVO_FINISH(TI, FA, EV)                                         \
-  {                                                                      \
-    const int orow_ = (TI) * 8 + g;                                      \
-    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;                   \
-    _Pragma("unroll") for (int u = 0; u < kShortK; ++u) {                \
-      if (u < nsteps) {                                                  \
-        dmma884(c00, c01, FA[u], fb0[u]);                                \
-        dmma884(c10, c11, FA[u], fb1[u]);                                \
-      }                                                                  \
-    }                                                                    \
-    dot_ktail(d, orow_, cA, cB, c00, c01, c10, c11);                     \
-    dot_store4<EK>(d, epi, orow_, cA, cB, c00, c01, c10, c11, EV);       \
-  }
-  GEVO_FETCH(w0, xa, xev);
-  for (int ti = w0; ti < tm; ti += 2 * wpc) {
-    const int t1 = ti + wpc, t2 = ti + 2 * wpc;
-    if (t1 < tm) GEVO_FETCH(t1, ya, yev);
-    GEVO_FINISH(ti, xa, xev);
-    if (t1 >= tm) break;
-    if (t2 < tm) GEVO_FETCH(t2, xa, xev);
-    GEVO_FINISH(t1, ya, yev);
-  }
-#undef GEVO_FETCH
-#undef GEVO_FINISH
-}
-
-__device__ void dot_direct(const gevo_instr& I, double* out, const double* A,
-                           const double* B, int ncols, const EpiDev* epi) {
-  DotGeom d;
-  d.M = I.shp[0];
-  d.K = I.aux[0];
-  d.ncols = ncols;
-  d.sam = I.in[0].st[0];
-  d.sak = I.in[0].st[1];
-  d.sbk = I.in[1].st[0];
-  d.sbn = I.in[1].st[1];
-  d.som = I.out.st[0];
-  d.son = I.out.st[1];
-  d.A = A + I.in[0].off;
-  d.B = B + I.in[1].off;
-  d.out = out + I.out.off;
-  const int tn = (ncols + 15) >> 4;
-  const int ek = !epi ? EK_NONE : (epi->fast == 1 ? EK_CHAIN : (epi->fast == 2 ? EK_SELECT : EK_GENERIC));
-  if (d.K <= 4 * kShortK + 3 && tn <= (int)(blockDim.x >> 5)) {
-    switch (ek) {
-      case EK_NONE: dot_short_k<EK_NONE>(d, epi); break;
-      case EK_CHAIN: dot_short_k<EK_CHAIN>(d, epi); break;
-      case EK_SELECT: dot_short_k<EK_SELECT>(d, epi); break;
-      default: dot_short_k<EK_GENERIC>(d, epi); break;
-    }
-  } else {
-    switch (ek) {
-      case EK_NONE: dot_long_k<EK_NONE>(d, epi); break;
-      case EK_CHAIN: dot_long_k<EK_CHAIN>(d, epi); break;
-      case EK_SELECT: dot_long_k<EK_SELECT>(d, epi); break;
-      default: dot_long_k<EK_GENERIC>(d, epi); break;
-    }
-  }
-}
+}  // namespace gevo
+#include "dot_staged.cuh"
+namespace gevo {
 
 __device__ __noinline__ void run_dot(Shared& S, const gevo_instr& I, double* stage) {
   const int n_ext = I.aux2[0];
@@ -648,41 +442,25 @@ __device__ __noinline__ void run_dot(Shared& S, const gevo_instr& I, double* sta
     __syncthreads();
     epi = &S.epi;
   }
-  double* out = opptr(S, I.out);
-  const double* A = opptr(S, I.in[0]);
-  const double* B = opptr(S, I.in[1]);
-  const int M = I.shp[0], N = I.shp[1], K = I.aux[0];
-  int split = I.aux[1];
-  const int64_t sam = I.in[0].st[0], sak = I.in[0].st[1];
-  const int64_t sbk = I.in[1].st[0], sbn = I.in[1].st[1];
-  const bool f = I.kin == GEVO_K_F64;
-  int first = 0;  // columns [0, first) done on the tensor path
-  if (f && I.sub == GEVO_D_FMA_CHAIN && split > 0) {
-    dot_direct(I, out, A, B, split, epi);
-    first = split;
-    if (first >= N) return;
-  }
-  const int span = N - first;
-  for (int e = threadIdx.x; e < M * span; e += blockDim.x) {
-    int i = e / span, j = first + (e - i * span);
-    const double* a = A + I.in[0].off + i * sam;
-    const double* b = B + I.in[1].off + j * sbn;
-    double r;
-    if (f) {
-      r = dot_elem(j < split ? I.sub : I.aux[2], a, sak, b, sbk, K);
-    } else {
-      uint64_t acc = 0;
-      for (int k = 0; k < K; ++k)
-        acc += (uint64_t)as_i64(a[k * sak]) * (uint64_t)as_i64(b[k * sbk]);
-      r = as_w((int64_t)acc);
-    }
-    if (epi) {
-      double evs[kEpiPre];
-      epi_fetch(*epi, i, j, evs);
-      r = epilogue(*epi, evs, r, i, j);
-    }
-    out[I.out.off + (int64_t)i * I.out.st[0] + (int64_t)j * I.out.st[1]] = r;
-  }
+  DotArgs d;
+  d.A = opptr(S, I.in[0]) + I.in[0].off;
+  d.B = opptr(S, I.in[1]) + I.in[1].off;
+  d.sam = I.in[0].st[0];
+  d.sak = I.in[0].st[1];
+  d.sbk = I.in[1].st[0];
+  d.sbn = I.in[1].st[1];
+  d.a_smem = I.in[0].buf == GEVO_BUF_SMEM;
+  d.b_smem = I.in[1].buf == GEVO_BUF_SMEM;
+  d.out = opptr(S, I.out) + I.out.off;
+  d.som = I.out.st[0];
+  d.son = I.out.st[1];
+  d.M = I.shp[0];
+  d.K = I.aux[0];
+  const int N = I.shp[1];
+  const bool integer = I.kin != GEVO_K_F64;
+  const int split = integer ? N : min(I.aux[1], N);
+  dot_columns(d, 0, split, I.sub, integer, stage, epi);
+  dot_columns(d, split, N, I.aux[2], integer, stage, epi);
 }
 
 // profile slot of an instruction: op class x sub-op x size bucket
@@ -691,7 +469,7 @@ __device__ __forceinline__ int prof_slot(const gevo_instr& I) {
   return ((I.op & 7) * 16 + (I.sub & 15)) * 2 + big;
 }
 
-__device__ void run_instrs(Shared& S, const gevo_instr* ins, int n, double* stage,
+__device__ __noinline__ void run_instrs(Shared& S, const gevo_instr* ins, int n, double* stage,
                            unsigned long long* prof) {
   long long t0 = 0;
   if (prof && threadIdx.x == 0) t0 = clock64();
@@ -741,6 +519,9 @@ eval_kernel(EvalArgs args) {
   double* dstage = dyn_smem;                // dot staging tiles
   double* smem_arena = dyn_smem + kStageElems;
   const gevo_prog P = args.progs[blockIdx.x];
+#ifdef GEVO_DOT_TIMING
+  if (threadIdx.x == 0) g_dot_prof = args.prof;
+#endif
   double* ind = args.arena + P.arena_off;
   const int wsz = (args.weight_elems + 15) & ~15;
   const int psz = (args.probs_elems + 15) & ~15;

@@ -64,4 +64,4 @@ def main(kind="small", n=256, steps=100):
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:2] or ["small"]))
+    main(sys.argv[1] if len(sys.argv) > 1 else "small", int(sys.argv[2]) if len(sys.argv) > 2 else 256)
