@@ -10,8 +10,10 @@ bench_train_pool.json.gz) -- real variant programs, not copies of one.
            plans resident; CUDA events on the launching stream, max over
            ranks)
   e2e    = individuals / wall time of the public API call
-           DeviceEvaluator.evaluate_variants (host lowering + plan H2D +
-           kernel + result D2H), plus the record all-gather when N > 1
+           DeviceEvaluator.evaluate_variants (host lowering in a process
+           pool, overlapped with the device: half the generation runs while
+           the other half is lowered; plan H2D + kernels + result D2H), plus
+           the record all-gather when N > 1
 
 `--impl reference` times the reference's algorithm on the host CPU (the
 oracle port, all cores, process pool), on the same workload.
@@ -253,13 +255,34 @@ def main():
         torch.cuda.synchronize()
 
     kern_ms, wall_s, alg_bytes, alg_flops, h2d, d2h = [], [], [], [], [], []
+    from paper_2310_10211_b200.evaluator import lower_all
+    from paper_2310_10211_b200.plan import build_population_plan
     clocks = Clocks(local)
+    # (1) value: plans built before timing; one launch per step on one
+    # context; device time of the evaluation kernel (CUDA events)
+    plans = []
+    for s in range(total_steps):
+        vps = [v for v in lower_all(batches[s][1], wl.config.cost_table, True) if v is not None]
+        plans.append(build_population_plan(vps, ev.weight_shapes, ev.batch * ev.classes))
     for s in range(total_steps):
         sel, fns = batches[s]
         flush.zero_()                       # L2 flush between iterations
         barrier()
         if s == args.warmup:
             clocks.start()
+        p = plans[s]
+        ev.ctx.eval(p.blob, p.n_prog, 0, steps_cfg, wl.config.finite_check_every, 0, 0,
+                    ev.weight_elems, False)
+        if s >= args.warmup:
+            kern_ms.append(ev.ctx.last_kernel_ms())
+            alg_bytes.append(sum(per_individual_bytes(f, steps_cfg, nb) for f in fns))
+            alg_flops.append(sum(per_individual_flops(f, steps_cfg, nb) for f in fns))
+    # (2) e2e: the public call on host data (lowering, plan H2D, kernels,
+    # results D2H; the record all-gather when N > 1), wall clock
+    for s in range(total_steps):
+        sel, fns = batches[s]
+        flush.zero_()
+        barrier()
         t0 = time.perf_counter()
         fits, recs = ev.evaluate_variants(fns, return_records=True)
         if world > 1:
@@ -267,10 +290,7 @@ def main():
             D.all_gather_records(loc, args.pop)
         t1 = time.perf_counter()
         if s >= args.warmup:
-            kern_ms.append(ev.ctx.last_kernel_ms())
             wall_s.append(t1 - t0)
-            alg_bytes.append(sum(per_individual_bytes(f, steps_cfg, nb) for f in fns))
-            alg_flops.append(sum(per_individual_flops(f, steps_cfg, nb) for f in fns))
             h2d.append(int(ev.last_plan_bytes))
             d2h.append(args.pop * 24)
     barrier()

@@ -28,6 +28,8 @@
  *   gevo_last_kernel_ms          -- (no analogue: device time of the last
  *                                   gevo_eval launch, CUDA events on the
  *                                   context's stream)
+ *   gevo_span_ms                 -- (no analogue: device span of a
+ *                                   generation split over two contexts)
  *
  * Conventions: every call returns 0 on success and a negative GEVO_E_* code
  * on failure (then gevo_last_error explains); no C++ exception crosses the
@@ -136,6 +138,11 @@ int gevo_profile(gevo_ctx* ctx, int enable, int64_t* out, int n);
 
 /* device milliseconds of the evaluation kernel of the last gevo_eval */
 int gevo_last_kernel_ms(gevo_ctx* ctx, double* ms);
+
+/* device milliseconds from the start of `first`'s last gevo_eval to the end
+ * of the later of the two contexts' last gevo_eval (one generation split in
+ * two halves over two contexts/streams of the same device) */
+int gevo_span_ms(gevo_ctx* first, gevo_ctx* second, double* ms);
 
 /* device and build info, e.g. "NVIDIA B200 sm_100 148 SMs" */
 int gevo_device_info(gevo_ctx* ctx, char* buf, size_t len);

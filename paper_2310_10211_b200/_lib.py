@@ -42,6 +42,7 @@ SIGNATURES = {
     "gevo_destroy": (ctypes.c_int, [ctypes.c_void_p]),
     "gevo_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),
     "gevo_last_kernel_ms": (ctypes.c_int, [ctypes.c_void_p, c_dblp]),
+    "gevo_span_ms": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, c_dblp]),
     "gevo_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_i64p, ctypes.c_int]),
     "gevo_device_info": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t]),
     "gevo_upload_split": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dblp,
@@ -89,6 +90,16 @@ def load():
 
 def ptr(a: np.ndarray, ctype=ctypes.c_double):
     return a.ctypes.data_as(ctypes.POINTER(ctype))
+
+
+def span_ms(first, second) -> float:
+    """Device milliseconds from the start of `first`'s last evaluation to the
+    end of whichever of the two contexts' last evaluations ended later."""
+    ms = ctypes.c_double()
+    rc = load().gevo_span_ms(first.h, second.h, ctypes.byref(ms))
+    if rc != 0:
+        raise GevoError(f"gevo_span_ms failed (rc={rc})")
+    return ms.value
 
 
 class Context:

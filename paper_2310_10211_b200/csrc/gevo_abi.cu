@@ -343,6 +343,18 @@ int gevo_last_kernel_ms(gevo_ctx* ctx, double* ms) {
   return GEVO_OK;
 }
 
+int gevo_span_ms(gevo_ctx* first, gevo_ctx* second, double* ms) {
+  if (!first || !second || !ms) return GEVO_E_ARG;
+  gevo_ctx* ctx = first;   // CK reports into the first context
+  if (first->device != second->device) return fail(ctx, GEVO_E_ARG, "contexts on different devices");
+  CK(cudaSetDevice(first->device));
+  float a = 0.f, b = 0.f;
+  CK(cudaEventElapsedTime(&a, first->ev0, first->ev1));
+  CK(cudaEventElapsedTime(&b, first->ev0, second->ev1));
+  *ms = a > b ? a : b;
+  return GEVO_OK;
+}
+
 int gevo_exec_once(gevo_ctx* ctx, const void* plan, size_t plan_bytes, const double* params,
                    size_t param_words, double* outs, size_t out_words) {
   if (!ctx) return GEVO_E_ARG;

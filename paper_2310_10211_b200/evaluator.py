@@ -13,6 +13,7 @@ Protocol restated from pkg/src/evotir/fitness.py:372-426:
 """
 from __future__ import annotations
 
+import os
 import time
 
 import numpy as np
@@ -24,6 +25,74 @@ from .workloads import (INVALID_FITNESS, PREDICTION, TRAINING, WEIGHT_NAMES,
 
 SPLIT_SEARCH, SPLIT_HOLDOUT = 0, 1
 STATUS_OK, STATUS_NONFINITE_WEIGHTS, STATUS_NONFINITE_PROBS = 0, 1, 2
+POOL_MIN = 32          # variants below which lowering stays in-process
+_POOL = None
+
+
+def _lower_pool():
+    """Process pool for host lowering (pure Python/numpy, GIL-bound): one
+    worker per core, created once.  Workers are forked (no re-import of
+    __main__) and only run lowering -- they never touch CUDA.
+    GEVO_B200_LOWER_WORKERS=1 disables it."""
+    global _POOL
+    if _POOL is None:
+        n = int(os.environ.get("GEVO_B200_LOWER_WORKERS", min(16, os.cpu_count() or 1)))
+        if n <= 1:
+            _POOL = False
+        else:
+            import multiprocessing as mp
+            import warnings
+            from concurrent.futures import ProcessPoolExecutor
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", DeprecationWarning)
+                _POOL = ProcessPoolExecutor(n, mp_context=mp.get_context("fork"))
+    return _POOL or None
+
+
+def _lower_many(batch):
+    """Worker: lower a list of variants; None for a variant that fails
+    (evaluate() maps any exception to INVALID_FITNESS)."""
+    fns_list, cost_table, training = batch
+    out = []
+    for fns in fns_list:
+        try:
+            out.append(lower_variant(fns, cost_table, training=training))
+        except Exception:
+            out.append(None)
+    return out
+
+
+def _submit_lowering(variants, idx, cost_table, training):
+    """Start lowering variants[idx] (None entries excluded by the caller).
+    Returns a list of (positions, future-or-result) in idx order."""
+    pool = _lower_pool() if len(idx) >= POOL_MIN else None
+    if pool is None:
+        return [(list(idx), _lower_many(([variants[i] for i in idx], cost_table, training)))]
+    nw = pool._max_workers
+    per = max(4, (len(idx) + 2 * nw - 1) // (2 * nw))
+    out = []
+    for k in range(0, len(idx), per):
+        c = idx[k:k + per]
+        out.append((c, pool.submit(_lower_many, ([variants[i] for i in c], cost_table, training))))
+    return out
+
+
+def _collect(jobs):
+    pos, res = [], []
+    for c, f in jobs:
+        pos.extend(c)
+        res.extend(f if isinstance(f, list) else f.result())
+    return pos, res
+
+
+def lower_all(variants, cost_table, training):
+    """lower_variant over a list (None entries stay None), in the process
+    pool when the list is large."""
+    idx = [i for i, v in enumerate(variants) if v is not None]
+    out = [None] * len(variants)
+    for i, r in zip(*_collect(_submit_lowering(variants, idx, cost_table, training))):
+        out[i] = r
+    return out
 
 
 class DeviceEvaluator:
@@ -49,15 +118,36 @@ class DeviceEvaluator:
         self.weight_shapes = [a.shape for a in w]
         self.ctx.upload_weights(np.concatenate([a.reshape(-1) for a in w]))
         self.weight_elems = int(sum(a.size for a in w))
+        self._flat_weights = np.concatenate([a.reshape(-1) for a in w])
+        self._ctx2 = None
         self.last_timing = {}
         self.last_plan_bytes = 0
+        self.last_device_ms = 0.0
+
+    def _second_context(self):
+        """A second context (own stream and buffers) on the same device: the
+        first half of a generation runs on one while the host lowers the
+        second half for the other."""
+        if self._ctx2 is None:
+            c = _lib.Context(self.device)
+            ds, cfg = self.workload.dataset, self.workload.config
+            c.upload_split(SPLIT_SEARCH, ds.search.x, ds.search.labels, cfg.classes,
+                           cfg.batch_size)
+            if self._holdout_batches is not None:
+                c.upload_split(SPLIT_HOLDOUT, ds.holdout.x, ds.holdout.labels,
+                               cfg.classes, cfg.batch_size)
+            c.upload_weights(self._flat_weights)
+            self._ctx2 = c
+        return self._ctx2
 
     def _ensure_holdout(self):
         if self._holdout_batches is None:
             ds, cfg = self.workload.dataset, self.workload.config
             ds.holdout.reads += 1      # the only reader of holdout (fitness.py:404)
-            self.ctx.upload_split(SPLIT_HOLDOUT, ds.holdout.x, ds.holdout.labels,
-                                  cfg.classes, cfg.batch_size)
+            for c in (self.ctx, self._ctx2):
+                if c is not None:
+                    c.upload_split(SPLIT_HOLDOUT, ds.holdout.x, ds.holdout.labels,
+                                   cfg.classes, cfg.batch_size)
             self._holdout_batches = len(ds.holdout.labels) // cfg.batch_size
         return self._holdout_batches
 
@@ -75,52 +165,79 @@ class DeviceEvaluator:
         if holdout and n_score == 0:
             from .workloads import WorkloadError
             raise WorkloadError("holdout split smaller than one batch")
-        lowered, slots = [], []
         fits = [None] * len(variants)
-        for i, fns in enumerate(variants):
-            if fns is None:
-                fits[i] = INVALID_FITNESS
-                continue
-            try:
-                vp = lower_variant(fns, cfg.cost_table, training=training)
-            except Exception:
-                fits[i] = INVALID_FITNESS      # evaluate(): any exception
-                continue
-            lowered.append(vp)
-            slots.append(i)
-        t1 = time.perf_counter()
+        idx = []
+        for i, v in enumerate(variants):
+            if v is None:
+                fits[i] = INVALID_FITNESS      # patch failed to apply
+            else:
+                idx.append(i)
         records = np.zeros(len(variants), dtype=_lib.RESULT_DTYPE)
-        finals = None
-        if lowered:
-            plan = build_population_plan(lowered, self.weight_shapes,
-                                         self.batch * self.classes)
-            t2 = time.perf_counter()
-            self.last_plan_bytes = plan.blob.nbytes
-            res, fw = self.ctx.eval(
-                plan.blob, plan.n_prog,
-                0 if training else 1, cfg.steps if training else 0,
-                cfg.finite_check_every, SPLIT_SEARCH,
-                SPLIT_HOLDOUT if holdout else SPLIT_SEARCH,
-                self.weight_elems, want_weights)
-            t3 = time.perf_counter()
-            if want_weights:
-                finals = [None] * len(variants)
+        finals = [None] * len(variants) if want_weights else None
+        split = SPLIT_HOLDOUT if holdout else SPLIT_SEARCH
+        # two halves when the pool is used: half A runs on the device (ctypes
+        # releases the GIL) while half B is still being lowered
+        halves = [idx]
+        if len(idx) >= 2 * POOL_MIN and _lower_pool() is not None:
+            halves = [idx[:len(idx) // 2], idx[len(idx) // 2:]]
+        jobs = [_submit_lowering(variants, h, cfg.cost_table, training) for h in halves]
+        ctxs = [self.ctx, self._second_context() if len(halves) > 1 else None]
+        runner, box = None, {}
+        t_lower = t_pack = 0.0
+        plan_bytes = 0
+        for h, job in enumerate(jobs):
+            ta = time.perf_counter()
+            pos, vps = _collect(job)
+            tb = time.perf_counter()
+            lowered, slots = [], []
+            for i, vp in zip(pos, vps):
+                if vp is None:
+                    fits[i] = INVALID_FITNESS  # evaluate(): any exception
+                else:
+                    lowered.append(vp)
+                    slots.append(i)
+            if not lowered:
+                continue
+            plan = build_population_plan(lowered, self.weight_shapes, self.batch * self.classes)
+            tc = time.perf_counter()
+            t_lower += tb - ta
+            t_pack += tc - tb
+            plan_bytes += plan.blob.nbytes
+            args = (plan.blob, plan.n_prog, 0 if training else 1, cfg.steps if training else 0,
+                    cfg.finite_check_every, SPLIT_SEARCH, split, self.weight_elems, want_weights)
+
+            def run(c=ctxs[h], a=args, key=h, lv=lowered, sl=slots):
+                box[key] = (c.eval(*a), lv, sl)
+            if h + 1 < len(jobs):
+                import threading
+                runner = threading.Thread(target=run)
+                runner.start()
+            else:
+                run()
+        if runner is not None:
+            runner.join()
+        used = sorted(box)
+        if len(used) == 2:
+            self.last_device_ms = _lib.span_ms(ctxs[0], ctxs[1])
+        elif used:
+            self.last_device_ms = ctxs[used[0]].last_kernel_ms()
+        for key in used:
+            (res, fw), lowered, slots = box[key]
             for k, vp in enumerate(lowered):
                 i = slots[k]
                 r = res[k]
                 records[i] = r
-                if training:
-                    cost = vp.train_cost * cfg.steps
-                else:
-                    cost = vp.fwd_cost * n_score
+                cost = vp.train_cost * cfg.steps if training else vp.fwd_cost * n_score
                 if r["status"] != STATUS_OK:
                     fits[i] = Fitness(cost, 1.0)
                 else:
                     fits[i] = Fitness(cost, int(r["wrong"]) / int(r["total"]))
                 if want_weights:
                     finals[i] = fw[k]
-            self.last_timing = {"lower_s": t1 - t0, "pack_s": t2 - t1,
-                                "device_s": t3 - t2, "n": len(lowered)}
+        self.last_plan_bytes = plan_bytes
+        self.last_timing = {"lower_wait_s": t_lower, "pack_s": t_pack,
+                            "total_s": time.perf_counter() - t0, "n": len(idx),
+                            "halves": len(halves)}
         out = [fits]
         if return_records:
             out.append(records)
@@ -147,6 +264,8 @@ class DeviceEvaluator:
 
     def close(self):
         self.ctx.close()
+        if self._ctx2 is not None:
+            self._ctx2.close()
 
 
 def baseline_functions(workload: Workload) -> dict:

@@ -22,6 +22,7 @@ order, so it is bit-identical.
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -200,7 +201,7 @@ class _Builder:
             "op": op, "sub": sub, "kout": out.kind,
             "kin": ins[0].kind if kin is None and ins else (kin or 0),
             "rank": len(shp) if rank is None else rank,
-            "n": int(np.prod(shp, dtype=np.int64)) if n is None else n,
+            "n": math.prod(shp) if n is None else n,
             "shp": _pad_dims(shp), "aux": list(aux or []) + [0] * (MAXR - len(aux or [])),
             "aux2": list(aux2 or []) + [0] * (MAXR - len(aux2 or [])),
             "out": out, "in": list(ins)}
@@ -248,7 +249,7 @@ class _Builder:
         """Storage for a materialised result: the OUT slot if it is returned
         (and dense in numpy's layout), else a fresh arena allocation."""
         r = self.direct.get(op.result)
-        count = int(np.prod(shape, dtype=np.int64)) if shape else 1
+        count = math.prod(shape)
         if r is not None and self.ret_layout == "c" and \
                 tuple(st) != L.c_strides(shape):
             r = None
@@ -360,7 +361,7 @@ class _Builder:
             return Val(a.buf, a.off, tuple(shape), st, a.kind, a.alloc)
         # numpy copies into C order, then reinterprets
         tmp = self.fresh(a.shape, L.c_strides(a.shape), a.kind,
-                         int(np.prod(a.shape, dtype=np.int64)))
+                         math.prod(a.shape))
         self.emit(OP_UNARY, U_COPY, tmp, [a])
         return Val(tmp.buf, tmp.off, tuple(shape), L.c_strides(shape),
                    tmp.kind, tmp.alloc)
@@ -466,9 +467,11 @@ def fuse_dot_epilogues(instrs):
             for k, v in enumerate(r.get("ext", [])):
                 if v.alloc >= 0:
                     readers.setdefault(v.alloc, []).append((i, k, "ext"))
-        merged = False
+        # merge every independent (dot, reader) pair found in this pass; an
+        # instruction takes part in at most one merge per pass
+        touched, drop = set(), []
         for i, d in enumerate(instrs):
-            if d["op"] != OP_DOT:
+            if d["op"] != OP_DOT or i in touched:
                 continue
             out = d["out"]
             if out.alloc < 0 or out.buf != BUF_ARENA:
@@ -478,7 +481,7 @@ def fuse_dot_epilogues(instrs):
                 continue
             j, k, _ = rs[0]
             r = instrs[j]
-            if j <= i or r["op"] not in (OP_UNARY, OP_BINARY, OP_SELECT):
+            if j <= i or j in touched or r["op"] not in (OP_UNARY, OP_BINARY, OP_SELECT):
                 continue
             if not _same_view(r["in"][k], out):
                 continue
@@ -499,11 +502,12 @@ def fuse_dot_epilogues(instrs):
             new = dict(d)
             new["epi"], new["ext"], new["out"] = epi, ext, r["out"]
             instrs[j] = new
-            del instrs[i]
-            merged = True
-            break
-        if not merged:
+            drop.append(i)
+            touched.update((i, j))
+        if not drop:
             return instrs
+        for i in reversed(drop):
+            del instrs[i]
 
 
 def lower_function(fn, param_layouts=None, ret_bufs=None, ret_layout="compact",
@@ -576,9 +580,20 @@ def _ext_records(rec):
     return out
 
 
+def _operand_words(v):
+    st = list(v.st)
+    return [v.buf, v.off] + st + [0] * (MAXR - len(st))
+
+
+_ZERO_OPERAND = [0] * (2 + MAXR)
+
+
 def encode_instrs(instrs, const_base=0) -> np.ndarray:
-    flat = []
+    """Instruction records -> gevo_instr array (one flat int32 list, then a
+    single array construction: 56 words per record, gevo_plan.h)."""
+    words = []
     for rec in instrs:
+        recs = [rec]
         if rec.get("epi"):
             exts = _ext_records(rec)
             rec = dict(rec)
@@ -586,34 +601,24 @@ def encode_instrs(instrs, const_base=0) -> np.ndarray:
             aux2[0] = len(exts)
             aux2[1] = len(rec["epi"])
             rec["aux2"] = aux2
-            flat.append(rec)
-            flat.extend(exts)
-        else:
-            flat.append(rec)
-    instrs = flat
-    arr = np.zeros(len(instrs), dtype=INSTR_DTYPE)
-    for i, rec in enumerate(instrs):
-        e = arr[i]
-        for k in ("op", "sub", "kout", "kin", "rank", "n"):
-            e[k] = rec[k]
-        e["shp"] = rec["shp"]
-        e["aux"] = rec["aux"]
-        e["aux2"] = rec["aux2"]
-        if rec["op"] in (OP_UNARY, OP_BINARY, OP_SELECT):
-            shape = tuple(rec["out"].shape)
-            modes = [_addr_mode(rec["out"], shape)]
-            modes += [_addr_mode(v, shape) for v in rec["in"]]
-            modes += [AM_SCALAR] * (4 - len(modes))
-            e["aux2"] = modes + [0] * (MAXR - 4)
-        for slot, v in [("out", rec["out"])]:
-            e[slot]["buf"] = v.buf
-            e[slot]["off"] = v.off
-            e[slot]["st"] = list(v.st) + [0] * (MAXR - len(v.st))
-        for j, v in enumerate(rec["in"]):
-            e["in"][j]["buf"] = v.buf
-            e["in"][j]["off"] = v.off
-            e["in"][j]["st"] = list(v.st) + [0] * (MAXR - len(v.st))
-    return arr
+            recs = [rec] + exts
+        for r in recs:
+            aux2 = r["aux2"]
+            ins = r["in"]
+            if r["op"] in (OP_UNARY, OP_BINARY, OP_SELECT):
+                shape = tuple(r["out"].shape)
+                modes = [_addr_mode(r["out"], shape)]
+                modes += [_addr_mode(v, shape) for v in ins]
+                aux2 = modes + [AM_SCALAR] * (4 - len(modes)) + [0] * (MAXR - 4)
+            words += [r["op"], r["sub"], r["kout"], r["kin"], r["rank"], r["n"]]
+            words += r["shp"]
+            words += r["aux"]
+            words += aux2
+            words += _operand_words(r["out"])
+            for j in range(3):
+                words += _operand_words(ins[j]) if j < len(ins) else _ZERO_OPERAND
+    arr = np.array(words, dtype=np.int32)
+    return arr.view(INSTR_DTYPE)
 
 
 def consts_to_words(consts) -> np.ndarray:

@@ -20,11 +20,12 @@ from .lowering import (BUF_OUT0, FLAG_LAYOUT_APPROX, HEADER_DTYPE,
 
 @dataclass
 class VariantPlan:
-    """Lowered functions of one individual."""
-    train0: list | None
-    train1: list | None
-    fwd: list
-    consts: list
+    """Lowered functions of one individual, already encoded (gevo_instr
+    arrays with CONST offsets relative to this individual's pool)."""
+    train0: np.ndarray | None
+    train1: np.ndarray | None     # same object as train0 when identical
+    fwd: np.ndarray
+    consts: np.ndarray            # 64-bit words
     arena: int
     smem: int
     flags: int
@@ -69,8 +70,8 @@ def lower_variant(functions: dict, cost_table=None, training=True,
                 layouts[:nw] = low1.ret_strides
                 low1 = lower_function(ts, layouts, cost_table=cost_table)
                 flags |= FLAG_LAYOUT_APPROX
-        t0 = _shift_consts(low0, consts)
-        t1 = t0 if low1 is low0 else _shift_consts(low1, consts)
+        t0 = _encode_shifted(low0, consts)
+        t1 = t0 if low1 is low0 else _encode_shifted(low1, consts)
         arena = max(low0.arena_elems, low1.arena_elems)
         smem = max(low0.smem_elems, low1.smem_elems)
         fwd_layouts = list(low1.ret_strides)
@@ -80,34 +81,25 @@ def lower_variant(functions: dict, cost_table=None, training=True,
     if fwd_layouts is not None:
         f_layout[:nwf] = fwd_layouts[:nwf]
     lowf = lower_function(fw, f_layout, ret_layout="c", cost_table=cost_table)
-    f = _shift_consts(lowf, consts)
+    f = _encode_shifted(lowf, consts)
     arena = max(arena, lowf.arena_elems)
     smem = max(smem, lowf.smem_elems)
-    return VariantPlan(t0, t1, f, consts, arena, smem, flags, train_cost, lowf.cost)
+    return VariantPlan(t0, t1, f, consts_to_words(consts), arena, smem, flags,
+                       train_cost, lowf.cost)
 
 
-def _shift_consts(low, pool):
-    """Append a function's constants to the individual's pool and rebase
-    its CONST operands."""
+def _encode_shifted(low, pool):
+    """Encode a function's instructions with its constants appended to the
+    individual's pool (CONST operand offsets rebased)."""
     base = len(pool)
     pool.extend(low.consts)
-    if base == 0:
-        return low.instrs
-    out = []
-    for rec in low.instrs:
-        rec = dict(rec)
-        rec["in"] = [_rebase(v, base) for v in rec["in"]]
-        if rec.get("ext"):
-            rec["ext"] = [_rebase(v, base) for v in rec["ext"]]
-        out.append(rec)
-    return out
-
-
-def _rebase(v, base):
-    if v.buf == 1:  # BUF_CONST
-        from .lowering import Val
-        return Val(v.buf, v.off + base, v.shape, v.st, v.kind, v.alloc)
-    return v
+    arr = encode_instrs(low.instrs)
+    if base:
+        for slot in ("out", "in"):
+            bufs = arr[slot]["buf"]
+            offs = arr[slot]["off"]
+            offs[bufs == 1] += base        # BUF_CONST
+    return arr
 
 
 @dataclass
@@ -141,21 +133,21 @@ def build_population_plan(variants: list[VariantPlan], weight_shapes,
         p = progs[slot]
         p["result_slot"] = idx
         p["const_off"] = n_const
-        const_chunks.append(consts_to_words(v.consts))
+        const_chunks.append(v.consts)
         n_const += len(v.consts)
         if v.train0 is not None:
-            a = encode_instrs(v.train0)
+            a = v.train0
             p["train0"], p["train0_n"] = n_instr, len(a)
             instr_chunks.append(a)
             n_instr += len(a)
             if v.train1 is v.train0:
                 p["train1"], p["train1_n"] = p["train0"], p["train0_n"]
             else:
-                b = encode_instrs(v.train1)
+                b = v.train1
                 p["train1"], p["train1_n"] = n_instr, len(b)
                 instr_chunks.append(b)
                 n_instr += len(b)
-        f = encode_instrs(v.fwd)
+        f = v.fwd
         p["fwd"], p["fwd_n"] = n_instr, len(f)
         instr_chunks.append(f)
         n_instr += len(f)

@@ -1,0 +1,88 @@
+"""Host logic of DeviceEvaluator without a GPU: the device context is
+replaced by a fake that records the plans it receives, so lowering (in-process
+and in the process pool), the two-half pipelined launch, result mapping and
+the reference's failure encodings are exercised on CPU."""
+import numpy as np
+import pytest
+
+from golden_io import load, variant_functions
+from paper_2310_10211_b200 import _lib, evaluator as E
+from paper_2310_10211_b200 import workloads as W
+from paper_2310_10211_b200.lowering import HEADER_DTYPE
+
+
+class FakeContext:
+    instances = []
+
+    def __init__(self, device=0):
+        self.plans = []
+        FakeContext.instances.append(self)
+
+    def upload_split(self, *a):
+        pass
+
+    def upload_weights(self, *a):
+        pass
+
+    def eval(self, blob, n_prog, mode, steps, check_every, train_split, score_split,
+             weight_elems=0, want_weights=False):
+        hdr = blob[:HEADER_DTYPE.itemsize].view(HEADER_DTYPE)[0]
+        assert hdr["n_prog"] == n_prog
+        self.plans.append(n_prog)
+        res = np.zeros(n_prog, dtype=_lib.RESULT_DTYPE)
+        # individual k: wrong = k, total = 992; every 7th blows up
+        res["wrong"] = np.arange(n_prog)
+        res["total"] = 992
+        res["status"][::7] = E.STATUS_NONFINITE_WEIGHTS
+        return res, None
+
+    def last_kernel_ms(self):
+        return 1.0
+
+    def close(self):
+        pass
+
+
+@pytest.fixture
+def fake(monkeypatch):
+    FakeContext.instances = []
+    monkeypatch.setattr(_lib, "Context", FakeContext)
+    monkeypatch.setattr(_lib, "span_ms", lambda a, b: 2.0)
+    return FakeContext
+
+
+@pytest.mark.parametrize("n", [5, 80])
+def test_evaluate_variants_maps_results_and_failures(fake, n):
+    wl = W.build_2fcnet_workload(W.WorkloadConfig(steps=60, dataset=W.DatasetConfig(
+        search_n=320, holdout_n=64)))
+    inds = load("train_pop.json.gz")["individuals"][:n]
+    variants = [variant_functions(i) for i in inds]
+    variants[1] = None                                  # a patch that failed to apply
+    ev = E.DeviceEvaluator(wl)
+    fits, recs = ev.evaluate_variants(variants, return_records=True)
+    assert fits[1] == W.INVALID_FITNESS
+    launched = sum(p for c in fake.instances for p in c.plans)
+    assert launched == n - 1
+    # pipelined halves when the process pool is used
+    assert ev.last_timing["halves"] == (2 if n >= 2 * E.POOL_MIN else 1)
+    for i, f in enumerate(fits):
+        if variants[i] is None:
+            continue
+        assert f.valid and f.cost > 0
+        if recs[i]["status"] != E.STATUS_OK:
+            assert f.error == 1.0                      # fitness.py:383-384
+        else:
+            assert f.error == recs[i]["wrong"] / 992
+    ev.close()
+
+
+def test_pool_lowering_matches_in_process():
+    inds = load("train_pop.json.gz")["individuals"][:70]
+    variants = [variant_functions(i) for i in inds]
+    a = E.lower_all(variants, None, True)             # pool (>= POOL_MIN)
+    b = E._lower_many((variants, None, True))         # in-process
+    for x, y in zip(a, b):
+        assert x.train_cost == y.train_cost and x.fwd_cost == y.fwd_cost
+        assert x.train0.tobytes() == y.train0.tobytes()
+        assert x.fwd.tobytes() == y.fwd.tobytes()
+        assert x.consts.tobytes() == y.consts.tobytes()
