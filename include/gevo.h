@@ -74,6 +74,8 @@ typedef struct {
   int64_t total;      /* scored examples (0 unless status OK) */
   int32_t status;     /* GEVO_STATUS_* */
   int32_t steps_run;  /* training steps executed before an early exit */
+  int64_t cycles;     /* SM clock cycles this individual's CTA ran (diagnostics:
+                         load balance, stragglers) */
 } gevo_result;
 
 typedef struct {

@@ -21,11 +21,13 @@ c_i64p = ctypes.POINTER(ctypes.c_int64)
 
 class GevoResult(ctypes.Structure):
     _fields_ = [("wrong", ctypes.c_int64), ("total", ctypes.c_int64),
-                ("status", ctypes.c_int32), ("steps_run", ctypes.c_int32)]
+                ("status", ctypes.c_int32), ("steps_run", ctypes.c_int32),
+                ("cycles", ctypes.c_int64)]
 
 
 RESULT_DTYPE = np.dtype([("wrong", "<i8"), ("total", "<i8"),
-                         ("status", "<i4"), ("steps_run", "<i4")])
+                         ("status", "<i4"), ("steps_run", "<i4"),
+                         ("cycles", "<i8")])
 
 
 class GevoEvalDesc(ctypes.Structure):

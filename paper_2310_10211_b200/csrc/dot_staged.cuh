@@ -636,8 +636,69 @@ __device__ unsigned long long* g_dot_prof;
 #define GEVO_TACC(p, a, b)
 #endif
 
+// One staged operand of dot_fast: whole aligned lines through a running
+// pointer (two 16-byte copies per thread per tile: lines t>>4 and t>>4 + 16 at
+// element 2*(t&15)), or, for any other strides / shared-memory sources, the
+// generic CopyPlan (kept in shared memory) with a (r0, k0) cursor.  Kept
+// small: it is live across the whole dot.
+struct Feed {
+  const double* p;     // vec: thread's copy 0 at the current stage
+  int so;              // vec: copy 1 = copy 0 + so
+  int adv;             // vec: advance per stage (elements)
+  int o0, r0, k0;      // generic: thread offset and tile origin
+  int flags;           // bit 0 vec, bit 1 lines along k
+};
+
+__device__ __forceinline__ int feed_rs(const Feed& f) { return (f.flags & 2) ? kTS : 1; }
+__device__ __forceinline__ int feed_ks(const Feed& f) { return (f.flags & 2) ? 1 : kTS; }
+
+__device__ __forceinline__ void feed_init(Feed& f, CopyPlan& cp, const double* p, int sr, int sk, bool smem,
+                                          int r0, int k0, int adv, int rext, int kext) {
+  const bool vec = !smem && vec_ok(p, sr, sk, rext, kext);
+  if (vec) {
+    const int ar = sr < 0 ? -sr : sr, ak = sk < 0 ? -sk : sk;
+    const bool kmaj = ak != 0 && (ar == 0 || ak <= ar);
+    const int cross = kmaj ? sr : sk;
+    const int t = threadIdx.x;
+    f.p = p + (int64_t)r0 * sr + (int64_t)k0 * sk + (int64_t)(t >> 4) * cross + (t & 15) * 2;
+    f.so = 16 * cross;
+    f.adv = adv;
+    f.flags = 1 | (kmaj ? 2 : 0);
+  } else {
+    if (threadIdx.x == 0) plan_init(cp, p, sr, sk, smem, false);
+    __syncthreads();
+    f.o0 = plan_o0(cp);
+    f.flags = cp_kmajor(cp) ? 2 : 0;
+  }
+  f.r0 = r0;
+  f.k0 = k0;
+}
+
+// stage the next tile (nr x nk valid); the generic cursor moves by (DR, DK)
+template <int DR, int DK>
+__device__ __forceinline__ void feed_stage(Feed& f, const CopyPlan& cp, uint32_t tile, int nr, int nk) {
+  if (f.flags & 1) {
+    const bool kmaj = f.flags & 2;
+    const int nline = kmaj ? nr : nk, nlen = kmaj ? nk : nr;
+    const int t = threadIdx.x, line0 = t >> 4, e = (t & 15) * 2;
+    if (e < nlen) {
+      const int bytes = nlen - e >= 2 ? 16 : 8;
+      const uint32_t d0 = tile + 8u * (line0 * kTS + e);
+      if (line0 < nline) cp_async16(d0, f.p, bytes);
+      if (line0 + 16 < nline) cp_async16(d0 + 8u * 16 * kTS, f.p + f.so, bytes);
+    }
+    f.p += f.adv;
+  } else {
+    stage(tile, cp, f.o0, f.r0, nr, f.k0, nk);
+    f.r0 += DR;
+    f.k0 += DK;
+  }
+}
+
+// Lean variant of dot_fast for the hot case: FMA chain, every operand whole
+// aligned lines (VecCopy only; nothing else live across the loop).
 template <bool PANELS>
-__device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, double* stage_buf,
+__device__ __noinline__ void dot_fast_vec(const DotArgs& dref, int col0, int col1, double* stage_buf,
                                       const EpiDev* epi) {
   const DotArgs d = dref;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -784,6 +845,234 @@ __device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, d
   cp_async_wait<0>();
 }
 
+// CK: 0 FMA_CHAIN, 1 ACC8 (8 lane chains (k mod 8) per output, each on its
+// own DMMA accumulator tile, chain j's four k of a chunk (j, j+8, j+16, j+24)
+// read from the unpermuted tile with stride 8; warp = one 8x8 tile, <= 16
+// columns), 2 SEQ_NOFMA, 3 integer (scalar; thread = 4 outputs of the panel).
+template <bool PANELS, int CK>
+__device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, double* stage_buf,
+                                      const EpiDev* epi, int mode) {
+  constexpr bool ACC8 = CK == 1;
+  constexpr bool SCALAR = CK >= 2;
+  const DotArgs d = dref;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int M = d.M, K = d.K, ncols = col1 - col0;
+  const int ek = !epi ? EK_NONE : (epi->fast == 1 ? EK_CHAIN : (epi->fast == 2 ? EK_SELECT : EK_GENERIC));
+  __shared__ EpiR R;
+  __shared__ CopyPlan cpa, cpx, cpb;
+  if (threadIdx.x == 0) epi_init(R, ek == EK_CHAIN || ek == EK_SELECT ? epi : nullptr, PANELS);
+  __syncthreads();
+  const bool etile = PANELS && R.tile >= 0;
+  const int total = PANELS ? (M + kPanel - 1) / kPanel : (K + kKC - 1) / kKC;
+  const uint32_t ring = smem_u32(stage_buf);
+  double* Bp = stage_buf + kDotStages * 2 * kTileElems;
+
+  // A; the second tile (B chunk for KSTREAM, epilogue operand for PANELS)
+  Feed fa, fx;
+  int brs, bks;
+  if (PANELS) {
+    feed_init(fa, cpa, d.A, d.sam, d.sak, d.a_smem, 0, 0, kPanel * d.sam, M, K);
+    if (etile)
+      feed_init(fx, cpx, R.ptr[R.tile], R.st0[R.tile], R.st1[R.tile], false, 0, col0, kPanel * R.st0[R.tile],
+                M, ncols);
+    else
+      fx.flags = 3;
+    // B (K x ncols) once, any layout
+    if (threadIdx.x == 0) plan_init(cpb, d.B + (int64_t)col0 * d.sbn, d.sbn, d.sbk, d.b_smem, false);
+    __syncthreads();
+    stage(smem_u32(Bp), cpb, plan_o0(cpb), 0, ncols, 0, K);
+    brs = cp_rs(cpb);
+    bks = cp_ks(cpb);
+  } else {
+    feed_init(fa, cpa, d.A, d.sam, d.sak, d.a_smem, 0, 0, kKC * d.sak, M, K);
+    feed_init(fx, cpx, d.B, d.sbn, d.sbk, d.b_smem, col0, 0, kKC * d.sbk, ncols, K);
+    brs = feed_rs(fx);
+    bks = feed_ks(fx);
+  }
+  const int ars = feed_rs(fa), aks = feed_ks(fa);
+  const int ers = feed_rs(fx), eks = feed_ks(fx);
+
+  // stage i covers rows [32i, ..) (PANELS) or k [32i, ..) (KSTREAM)
+  auto load = [&](int i, int slot) {
+    const uint32_t As = ring + 8u * (slot * 2 * kTileElems);
+    if (PANELS) {
+      const int pm = min(kPanel, M - i * kPanel);
+      feed_stage<kPanel, 0>(fa, cpa, As, pm, K);
+      if (etile) feed_stage<kPanel, 0>(fx, cpx, As + 8u * kTileElems, pm, ncols);
+    } else {
+      const int nk = min(kKC, K - i * kKC);
+      feed_stage<0, kKC>(fa, cpa, As, M, nk);
+      feed_stage<0, kKC>(fx, cpx, As + 8u * kTileElems, ncols, nk);
+    }
+  };
+#pragma unroll 1
+  for (int i = 0; i < kDotStages - 1; ++i) {
+    if (i < total) load(i, i);
+    cp_async_commit();
+  }
+  const int rb = warp >> 1, cb0 = ACC8 ? (warp & 1) : (warp & 1) * 2;
+  const int lm = rb * 8 + g, ln = cb0 * 8 + 2 * t4;
+  const int kmain = (ACC8 && mode == GEVO_D_ACC8_TAIL) ? (K & ~7) : K;
+  constexpr int NACC = ACC8 ? 16 : 4;
+  double acc[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+  int slot = 0, lslot = kDotStages - 1;
+#pragma unroll 1
+  for (int s = 0; s < total; ++s) {
+    GEVO_TSTAMP(ta)
+    if (s + kDotStages - 1 < total) load(s + kDotStages - 1, lslot);
+    cp_async_commit();
+    GEVO_TSTAMP(tl)
+    cp_async_wait<kDotStages - 1>();
+    __syncthreads();
+    GEVO_TSTAMP(tb)
+    GEVO_TACC(1, ta, tl)
+    GEVO_TACC(2, tl, tb)
+    double* As = stage_buf + slot * 2 * kTileElems;
+    const double* Bs = PANELS ? Bp : As + kTileElems;
+    const int pm = PANELS ? min(kPanel, M - s * kPanel) : M;
+    const int nk = PANELS ? K : min(kKC, K - s * kKC);    const bool last = PANELS || s == total - 1;
+    const bool act0 = !SCALAR && rb * 8 < pm && cb0 * 8 < ncols;
+    const bool act1 = !ACC8 && act0 && (cb0 + 1) * 8 < ncols;
+    if (SCALAR) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int o = threadIdx.x + u * kDotThreads;
+        const int mm = o >> 5, nn = o & 31;
+        if (mm < pm && nn < ncols) {
+          const double* pa = As + mm * ars;
+          const double* pb = Bs + nn * brs;
+          double v = acc[u];
+          if (CK == 2) {
+#pragma unroll 4
+            for (int kk = 0; kk < nk; ++kk) v = __dadd_rn(v, __dmul_rn(pa[kk * aks], pb[kk * bks]));
+          } else {
+            uint64_t w = (uint64_t)as_i64(v);
+#pragma unroll 4
+            for (int kk = 0; kk < nk; ++kk)
+              w += (uint64_t)as_i64(pa[kk * aks]) * (uint64_t)as_i64(pb[kk * bks]);
+            v = as_w((int64_t)w);
+          }
+          acc[u] = v;
+        }
+      }
+    }
+    if (ACC8 && act0) {
+      const int k0 = PANELS ? 0 : s * kKC;
+      const double* pa = As + lm * ars + 8 * t4 * aks;
+      const double* pb = Bs + (cb0 * 8 + g) * brs + 8 * t4 * bks;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (k0 + j + 24 < kmain) {
+          dmma884(acc[2 * j], acc[2 * j + 1], pa[j * aks], pb[j * bks]);
+        } else {
+#pragma unroll 1
+          for (int t = 0; t < 4; ++t) {
+            const int kk = j + 8 * t;
+            if (k0 + kk >= kmain) break;
+            const double a = As[lm * ars + kk * aks];
+            acc[2 * j] = fma(a, Bs[ln * brs + kk * bks], acc[2 * j]);
+            acc[2 * j + 1] = fma(a, Bs[(ln + 1) * brs + kk * bks], acc[2 * j + 1]);
+          }
+        }
+      }
+      if (last) {
+        // pairwise lane tree, then (ACC8_TAIL) the fma tail over k >= K&~7
+        double r0 = __dadd_rn(__dadd_rn(__dadd_rn(acc[0], acc[2]), __dadd_rn(acc[4], acc[6])),
+                              __dadd_rn(__dadd_rn(acc[8], acc[10]), __dadd_rn(acc[12], acc[14])));
+        double r1 = __dadd_rn(__dadd_rn(__dadd_rn(acc[1], acc[3]), __dadd_rn(acc[5], acc[7])),
+                              __dadd_rn(__dadd_rn(acc[9], acc[11]), __dadd_rn(acc[13], acc[15])));
+#pragma unroll 1
+        for (int kk = kmain - k0; kk < nk; ++kk) {
+          const double a = As[lm * ars + kk * aks];
+          r0 = fma(a, Bs[ln * brs + kk * bks], r0);
+          r1 = fma(a, Bs[(ln + 1) * brs + kk * bks], r1);
+        }
+#pragma unroll
+        for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+        acc[0] = r0;
+        acc[1] = r1;
+      }
+    } else if (!ACC8 && act0) {
+      const double* pa = As + lm * ars + t4 * aks;
+      const double* pb0 = Bs + (cb0 * 8 + g) * brs + t4 * bks;
+      const double* pb1 = pb0 + 8 * brs;
+      const int nq = nk >> 2;
+      const int qa = 4 * aks, qb = 4 * bks;
+      if (nq == 8 && act1) {
+        // all 24 fragments first (one LDS latency), then 16 back-to-back DMMAs
+        double fa[8], fb0[8], fb1[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          fa[q] = pa[q * qa];
+          fb0[q] = pb0[q * qb];
+          fb1[q] = pb1[q * qb];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          dmma884(acc[0], acc[1], fa[q], fb0[q]);
+          dmma884(acc[2], acc[3], fa[q], fb1[q]);
+        }
+      } else {
+#pragma unroll 1
+        for (int q = 0; q < nq; ++q) {
+          const double a = pa[q * qa];
+          dmma884(acc[0], acc[1], a, pb0[q * qb]);
+          if (act1) dmma884(acc[2], acc[3], a, pb1[q * qb]);
+        }
+#pragma unroll 1
+        for (int kk = nq * 4; kk < nk; ++kk) {
+          const double a = As[lm * ars + kk * aks];
+          acc[0] = fma(a, Bs[ln * brs + kk * bks], acc[0]);
+          acc[1] = fma(a, Bs[(ln + 1) * brs + kk * bks], acc[1]);
+          if (act1) {
+            acc[2] = fma(a, Bs[(ln + 8) * brs + kk * bks], acc[2]);
+            acc[3] = fma(a, Bs[(ln + 9) * brs + kk * bks], acc[3]);
+          }
+        }
+      }
+    }
+    GEVO_TSTAMP(tc)
+    GEVO_TACC(3, tb, tc)
+    if (last) {
+      __syncthreads();                // A consumed: its region becomes the C tile
+      double* Cs = As;
+      if (SCALAR) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int o = threadIdx.x + u * kDotThreads;
+          Cs[(o >> 5) * kCS + (o & 31)] = acc[u];
+        }
+      } else if (act0) {
+        Cs[lm * kCS + ln] = acc[0];
+        Cs[lm * kCS + ln + 1] = acc[1];
+        if (!ACC8) {
+          Cs[lm * kCS + ln + 8] = acc[2];
+          Cs[lm * kCS + ln + 9] = acc[3];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+      __syncthreads();
+      const int m0 = PANELS ? s * kPanel : 0;
+      GEVO_TSTAMP(te0)
+      GEVO_TACC(4, tc, te0)
+      dot_emit_dispatch<0>(ek, Cs, As + kTileElems, R, ers, eks, epi, d.out, d.som, d.son, m0, col0, pm, ncols);
+      GEVO_TSTAMP(te1)
+      GEVO_TACC(5, te0, te1)
+    }
+    slot = slot + 1 == kDotStages ? 0 : slot + 1;
+    lslot = lslot + 1 == kDotStages ? 0 : lslot + 1;
+    GEVO_TSTAMP(tf0)
+    __syncthreads();
+    GEVO_TSTAMP(tf1)
+    GEVO_TACC(6, tf0, tf1)
+  }
+  cp_async_wait<0>();
+}
+
 // PANELS needs its tile-staged epilogue operand (the first full-matrix one,
 // see epi_init) to be made of whole aligned lines
 __device__ __forceinline__ bool dot_etile_ok(const EpiDev* e, int ncols, int M) {
@@ -798,21 +1087,46 @@ __device__ __forceinline__ bool dot_etile_ok(const EpiDev* e, int ncols, int M) 
 __device__ __forceinline__ void dot_columns(const DotArgs& d, int col0, int col1, int mode, bool integer,
                                             double* stage_buf, const EpiDev* epi) {
   if (col0 >= col1) return;
-  if (integer) dot_run<3>(d, col0, col1, mode, stage_buf, epi);
-  else if (mode == GEVO_D_SEQ_NOFMA) dot_run<2>(d, col0, col1, mode, stage_buf, epi);
-  else if (mode == GEVO_D_FMA_CHAIN) {
-    const int ncols = col1 - col0;
-    const bool a_ok = !d.a_smem && vec_ok(d.A, d.sam, d.sak, d.M, d.K);
-    if (ncols <= kPanel && d.M <= kPanel && d.K > kKC && a_ok && !d.b_smem &&
-        vec_ok(d.B + (int64_t)col0 * d.sbn, d.sbn, d.sbk, ncols, d.K)) {
-      dot_fast<false>(d, col0, col1, stage_buf, epi);
-    } else if (ncols <= kPanel && d.K <= kKC && a_ok && (!epi || epi->fast == 0 || dot_etile_ok(epi, ncols, d.M))) {
-      dot_fast<true>(d, col0, col1, stage_buf, epi);
-    } else {
-      dot_run<0>(d, col0, col1, mode, stage_buf, epi);
+  // fast paths (one <= 32-row panel with K streamed, or K <= 32 with rows
+  // streamed), in column pieces of <= 32 (<= 16 for ACC8); the general
+  // pipeline otherwise
+  const int ck = integer ? 3 : (mode == GEVO_D_SEQ_NOFMA ? 2 : (mode == GEVO_D_FMA_CHAIN ? 0 : 1));
+  const int width = ck == 1 ? 16 : kPanel;
+  const bool kstream = d.M <= kPanel && d.K > kKC;
+  const bool panels = d.K <= kKC && (!epi || epi->fast == 0 || dot_etile_ok(epi, col1 - col0, d.M));
+  if (kstream || panels) {
+    for (int c = col0; c < col1; c += width) {
+      const int c1 = min(c + width, col1);
+      if (ck == 0 && !d.a_smem && vec_ok(d.A, d.sam, d.sak, d.M, d.K) &&
+          (kstream ? (!d.b_smem && vec_ok(d.B + (int64_t)c * d.sbn, d.sbn, d.sbk, c1 - c, d.K)) : true)) {
+        if (kstream) dot_fast_vec<false>(d, c, c1, stage_buf, epi);
+        else dot_fast_vec<true>(d, c, c1, stage_buf, epi);
+        continue;
+      }
+      if (kstream) {
+        switch (ck) {
+          case 0: dot_fast<false, 0>(d, c, c1, stage_buf, epi, mode); break;
+          case 1: dot_fast<false, 1>(d, c, c1, stage_buf, epi, mode); break;
+          case 2: dot_fast<false, 2>(d, c, c1, stage_buf, epi, mode); break;
+          default: dot_fast<false, 3>(d, c, c1, stage_buf, epi, mode); break;
+        }
+      } else {
+        switch (ck) {
+          case 0: dot_fast<true, 0>(d, c, c1, stage_buf, epi, mode); break;
+          case 1: dot_fast<true, 1>(d, c, c1, stage_buf, epi, mode); break;
+          case 2: dot_fast<true, 2>(d, c, c1, stage_buf, epi, mode); break;
+          default: dot_fast<true, 3>(d, c, c1, stage_buf, epi, mode); break;
+        }
+      }
     }
+    return;
   }
-  else dot_run<1>(d, col0, col1, mode, stage_buf, epi);
+  switch (ck) {
+    case 0: dot_run<0>(d, col0, col1, mode, stage_buf, epi); break;
+    case 1: dot_run<1>(d, col0, col1, mode, stage_buf, epi); break;
+    case 2: dot_run<2>(d, col0, col1, mode, stage_buf, epi); break;
+    default: dot_run<3>(d, col0, col1, mode, stage_buf, epi); break;
+  }
 }
 
 }  // namespace gevo

@@ -60,17 +60,7 @@ __device__ __forceinline__ double* opptr(const Shared& S, const gevo_operand& o)
 // thread keeps kEwUnroll independent elements in flight for memory-level
 // parallelism.
 // ---------------------------------------------------------------------------
-constexpr int kEwUnroll = 8;
-
-struct EwDesc {
-  double* out;
-  const double* in[3];
-  int off[4];          // out, in0, in1, in2 (element offsets)
-  int step[4];         // linear mode: 1 (C order) or 0 (scalar)
-  int sr[4], sc[4];    // 2-D mode: row / column strides
-  int n, rank, C;
-  int mode;            // 0 linear, 1 2-D (rank <= 2), 2 generic unravel
-};
+constexpr int kEwUnroll = 4;
 
 struct FAdd { __device__ double operator()(double a, double b, double) const { return __dadd_rn(a, b); } };
 struct FSub { __device__ double operator()(double a, double b, double) const { return __dsub_rn(a, b); } };
@@ -91,138 +81,118 @@ struct FUnGeneric {
   __device__ double operator()(double a, double, double) const { return apply_unary(sub, kin, kout, a); }
 };
 
-// every operand C-ordered like the output (or a scalar): address = off + i*step
+// One elementwise instruction, read straight from the (shared-memory cached)
+// record: addressing per operand from aux2 (AM_LINEAR / AM_SCALAR: address
+// off + i*step; otherwise rank <= 2 walked as (row, col) incrementally, or a
+// generic unravel).  One out-of-line instance per functor.
 template <int NIN, class F>
-__device__ __forceinline__ void ew_linear(const EwDesc& d, F f) {
-  for (int base = threadIdx.x; base < d.n; base += kEwUnroll * kThreads) {
-    double a[kEwUnroll], b[kEwUnroll], c[kEwUnroll];
-#pragma unroll
-    for (int u = 0; u < kEwUnroll; ++u) {
-      const int i = base + u * kThreads;
-      if (i < d.n) {
-        a[u] = d.in[0][d.off[1] + i * d.step[1]];
-        if (NIN > 1) b[u] = d.in[1][d.off[2] + i * d.step[2]];
-        if (NIN > 2) c[u] = d.in[2][d.off[3] + i * d.step[3]];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kEwUnroll; ++u) {
-      const int i = base + u * kThreads;
-      if (i < d.n) d.out[d.off[0] + i * d.step[0]] = f(a[u], NIN > 1 ? b[u] : 0.0, NIN > 2 ? c[u] : 0.0);
-    }
-  }
-}
-
-// rank <= 2, any strides: element i = (r, c) walked incrementally (no
-// division per element)
-template <int NIN, class F>
-__device__ __forceinline__ void ew_2d(const EwDesc& d, F f) {
-  const int C = d.C;
-  const int q = kThreads / C, rm = kThreads - q * C;
-  int r = threadIdx.x / C, c = threadIdx.x - (threadIdx.x / C) * C;
-  for (int base = threadIdx.x; base < d.n; base += kEwUnroll * kThreads) {
-    double a[kEwUnroll], b[kEwUnroll], x[kEwUnroll];
-    int ao[kEwUnroll];
-#pragma unroll
-    for (int u = 0; u < kEwUnroll; ++u) {
-      if (base + u * kThreads < d.n) {
-        ao[u] = d.off[0] + r * d.sr[0] + c * d.sc[0];
-        a[u] = d.in[0][d.off[1] + r * d.sr[1] + c * d.sc[1]];
-        if (NIN > 1) b[u] = d.in[1][d.off[2] + r * d.sr[2] + c * d.sc[2]];
-        if (NIN > 2) x[u] = d.in[2][d.off[3] + r * d.sr[3] + c * d.sc[3]];
-      }
-      c += rm;
-      r += q;
-      if (c >= C) { c -= C; ++r; }
-    }
-#pragma unroll
-    for (int u = 0; u < kEwUnroll; ++u)
-      if (base + u * kThreads < d.n) d.out[ao[u]] = f(a[u], NIN > 1 ? b[u] : 0.0, NIN > 2 ? x[u] : 0.0);
-  }
-}
-
-template <int NIN, class F>
-__device__ __forceinline__ void ew_unravel(const gevo_instr& I, const EwDesc& d, F f) {
+__device__ __noinline__ void ew_instr(const Shared& S, const gevo_instr& I, F f) {
+  const int n = I.n;
   const gevo_operand* ops[4] = {&I.out, &I.in[0], &I.in[1], &I.in[2]};
-  const int rank = d.rank;
-  for (int i = threadIdx.x; i < d.n; i += kThreads) {
+  double* out = S.base[I.out.buf];
+  const double* in0 = S.base[I.in[0].buf];
+  const double* in1 = NIN > 1 ? S.base[I.in[1].buf] : in0;
+  const double* in2 = NIN > 2 ? S.base[I.in[2].buf] : in0;
+  int off[4], step[4];
+  bool strided = false;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int am = k <= NIN ? I.aux2[k] : AM_SCALAR;
+    off[k] = k <= NIN ? ops[k]->off : 0;
+    step[k] = am == AM_LINEAR ? 1 : 0;
+    strided |= am == AM_STRIDED;
+  }
+  if (!strided) {
+    for (int base = threadIdx.x; base < n; base += kEwUnroll * kThreads) {
+      double a[kEwUnroll], b[kEwUnroll], c[kEwUnroll];
+#pragma unroll
+      for (int u = 0; u < kEwUnroll; ++u) {
+        const int i = base + u * kThreads;
+        if (i < n) {
+          a[u] = in0[off[1] + i * step[1]];
+          if (NIN > 1) b[u] = in1[off[2] + i * step[2]];
+          if (NIN > 2) c[u] = in2[off[3] + i * step[3]];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kEwUnroll; ++u) {
+        const int i = base + u * kThreads;
+        if (i < n) out[off[0] + i * step[0]] = f(a[u], NIN > 1 ? b[u] : 0.0, NIN > 2 ? c[u] : 0.0);
+      }
+    }
+    return;
+  }
+  const int rank = I.rank;
+  if (rank <= 2) {
+    int sr[4], sc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      sr[k] = k <= NIN && rank == 2 ? ops[k]->st[0] : 0;
+      sc[k] = k <= NIN && rank >= 1 ? ops[k]->st[rank - 1] : 0;
+    }
+    const int C = rank == 2 ? I.shp[1] : (rank == 1 ? I.shp[0] : 1);
+    const int q = kThreads / C, rm = kThreads - q * C;
+    int r = threadIdx.x / C, c = threadIdx.x - r * C;
+    for (int base = threadIdx.x; base < n; base += kEwUnroll * kThreads) {
+      double a[kEwUnroll], b[kEwUnroll], x[kEwUnroll];
+      int ao[kEwUnroll];
+#pragma unroll
+      for (int u = 0; u < kEwUnroll; ++u) {
+        if (base + u * kThreads < n) {
+          ao[u] = off[0] + r * sr[0] + c * sc[0];
+          a[u] = in0[off[1] + r * sr[1] + c * sc[1]];
+          if (NIN > 1) b[u] = in1[off[2] + r * sr[2] + c * sc[2]];
+          if (NIN > 2) x[u] = in2[off[3] + r * sr[3] + c * sc[3]];
+        }
+        c += rm;
+        r += q;
+        if (c >= C) { c -= C; ++r; }
+      }
+#pragma unroll
+      for (int u = 0; u < kEwUnroll; ++u)
+        if (base + u * kThreads < n) out[ao[u]] = f(a[u], NIN > 1 ? b[u] : 0.0, NIN > 2 ? x[u] : 0.0);
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < n; i += kThreads) {
     int idx[GEVO_MAXR];
     unravel(i, rank, I.shp, idx);
     int64_t ad[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      int64_t v = d.off[k];
+      int64_t v = off[k];
       if (k <= NIN)
-        for (int r = 0; r < rank; ++r) v += (int64_t)idx[r] * ops[k]->st[r];
+        for (int d = 0; d < rank; ++d) v += (int64_t)idx[d] * ops[k]->st[d];
       ad[k] = v;
     }
-    const double a = d.in[0][ad[1]];
-    const double b = NIN > 1 ? d.in[1][ad[2]] : 0.0;
-    const double c = NIN > 2 ? d.in[2][ad[3]] : 0.0;
-    d.out[ad[0]] = f(a, b, c);
+    const double a = in0[ad[1]];
+    const double b = NIN > 1 ? in1[ad[2]] : 0.0;
+    const double c = NIN > 2 ? in2[ad[3]] : 0.0;
+    out[ad[0]] = f(a, b, c);
   }
 }
 
-// (d is copied into registers: through the reference, every store to d.out
-// could alias the caller's descriptor and would force a reload)
-template <int NIN, class F>
-__device__ __noinline__ void ew_run(const gevo_instr& I, const EwDesc& dref, F f) {
-  const EwDesc d = dref;
-  if (d.mode == 0) ew_linear<NIN>(d, f);
-  else if (d.mode == 1) ew_2d<NIN>(d, f);
-  else ew_unravel<NIN>(I, d, f);
-}
-
-__device__ __noinline__ void run_elementwise(const Shared& S, const gevo_instr& I) {
-  EwDesc d;
-  const int op = I.op;
-  d.n = I.n;
-  d.rank = I.rank;
-  d.out = opptr(S, I.out);
-  d.off[0] = I.out.off;
-  const int nin = op == GEVO_OP_UNARY ? 1 : (op == GEVO_OP_BINARY ? 2 : 3);
-  bool strided = I.aux2[0] == AM_STRIDED;
-  d.step[0] = I.aux2[0] == AM_LINEAR ? 1 : 0;
-  const gevo_operand* ops[4] = {&I.out, &I.in[0], &I.in[1], &I.in[2]};
-  for (int k = 0; k < 3; ++k) {
-    if (k < nin) {
-      d.in[k] = opptr(S, I.in[k]);
-      d.off[k + 1] = I.in[k].off;
-      d.step[k + 1] = I.aux2[k + 1] == AM_LINEAR ? 1 : 0;
-      strided |= I.aux2[k + 1] == AM_STRIDED;
-    } else {
-      d.in[k] = d.in[0];
-      d.off[k + 1] = 0;
-      d.step[k + 1] = 0;
-    }
-  }
-  d.mode = !strided ? 0 : (d.rank <= 2 ? 1 : 2);
-  d.C = d.rank == 2 ? I.shp[1] : (d.rank == 1 ? I.shp[0] : 1);
-  for (int k = 0; k < 4; ++k) {
-    const bool used = k <= nin;
-    d.sr[k] = used && d.rank == 2 ? ops[k]->st[0] : 0;
-    d.sc[k] = used && d.rank >= 1 ? ops[k]->st[d.rank - 1] : 0;
-  }
-  const int kin = I.kin, sub = I.sub;
-  if (op == GEVO_OP_SELECT) { ew_run<3>(I, d, FSel()); return; }
+__device__ __forceinline__ void run_elementwise(const Shared& S, const gevo_instr& I) {
+  const int op = I.op, kin = I.kin, sub = I.sub;
+  if (op == GEVO_OP_SELECT) { ew_instr<3>(S, I, FSel()); return; }
   if (op == GEVO_OP_UNARY) {
-    if (sub == GEVO_U_COPY) { ew_run<1>(I, d, FCopy()); return; }
-    if (kin == GEVO_K_F64 && sub == GEVO_U_EXP) { ew_run<1>(I, d, FExp()); return; }
-    if (kin == GEVO_K_F64 && sub == GEVO_U_NEG) { ew_run<1>(I, d, FNeg()); return; }
-    ew_run<1>(I, d, FUnGeneric{sub, kin, I.kout});
+    if (sub == GEVO_U_COPY) { ew_instr<1>(S, I, FCopy()); return; }
+    if (kin == GEVO_K_F64 && sub == GEVO_U_EXP) { ew_instr<1>(S, I, FExp()); return; }
+    if (kin == GEVO_K_F64 && sub == GEVO_U_NEG) { ew_instr<1>(S, I, FNeg()); return; }
+    ew_instr<1>(S, I, FUnGeneric{sub, kin, I.kout});
     return;
   }
   if (kin == GEVO_K_F64) {
     switch (sub) {
-      case GEVO_B_ADD: ew_run<2>(I, d, FAdd()); return;
-      case GEVO_B_SUB: ew_run<2>(I, d, FSub()); return;
-      case GEVO_B_MUL: ew_run<2>(I, d, FMul()); return;
-      case GEVO_B_DIV: ew_run<2>(I, d, FDiv()); return;
-      case GEVO_B_MAX: ew_run<2>(I, d, FMax()); return;
-      case GEVO_B_GT: ew_run<2>(I, d, FGt()); return;
+      case GEVO_B_ADD: ew_instr<2>(S, I, FAdd()); return;
+      case GEVO_B_SUB: ew_instr<2>(S, I, FSub()); return;
+      case GEVO_B_MUL: ew_instr<2>(S, I, FMul()); return;
+      case GEVO_B_DIV: ew_instr<2>(S, I, FDiv()); return;
+      case GEVO_B_MAX: ew_instr<2>(S, I, FMax()); return;
+      case GEVO_B_GT: ew_instr<2>(S, I, FGt()); return;
     }
   }
-  ew_run<2>(I, d, FBinGeneric{sub, kin});
+  ew_instr<2>(S, I, FBinGeneric{sub, kin});
 }
 
 __device__ __noinline__ void run_pad(const Shared& S, const gevo_instr& I) {
@@ -532,6 +502,7 @@ eval_kernel(EvalArgs args) {
   const int nw = args.n_weights;
   int status = GEVO_STATUS_OK;
   int steps_run = 0;
+  const long long t_start = clock64();
 
   const double* final_w = args.init_weights;
   if (args.mode == GEVO_MODE_TRAIN && args.steps > 0) {
@@ -609,6 +580,7 @@ eval_kernel(EvalArgs args) {
     R->total = status == GEVO_STATUS_OK ? total : 0;
     R->status = status;
     R->steps_run = steps_run;
+    R->cycles = clock64() - t_start;
   }
   if (args.final_weights != nullptr) {
     double* dst = args.final_weights + (int64_t)P.result_slot * args.weight_elems;

@@ -16,6 +16,7 @@ evaluator (genome.py:511-515), so inputs here are already well typed.
 from __future__ import annotations
 
 import re
+import copyreg
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -72,6 +73,26 @@ class FunctionBody:
 class Module:
     functions: dict
     constants: dict = field(default_factory=dict)  # name -> ndarray
+
+
+# Compact pickling (positional tuples instead of dataclass __dict__s): the
+# evaluator ships variant functions to its lowering processes, and this is
+# the part of that transfer the parent pays serially.
+def _reduce_type(t):
+    return (TensorType, (t.shape, t.kind))
+
+
+def _reduce_op(o):
+    return (Operation, (o.op_id, o.opcode, o.result, o.result_type, o.operands, o.attrs))
+
+
+def _reduce_fn(f):
+    return (FunctionBody, (f.name, f.params, f.ops, f.returns, f.return_types))
+
+
+copyreg.pickle(TensorType, _reduce_type)
+copyreg.pickle(Operation, _reduce_op)
+copyreg.pickle(FunctionBody, _reduce_fn)
 
 
 def kind_name(kind) -> str:

@@ -26,7 +26,8 @@ class TableBackend:
         from paper_2310_10211_b200.workloads import Fitness, INVALID_FITNESS
         fits = []
         recs = np.zeros(len(variants), dtype=[("wrong", "<i8"), ("total", "<i8"),
-                                               ("status", "<i4"), ("steps_run", "<i4")])
+                                               ("status", "<i4"), ("steps_run", "<i4"),
+                                               ("cycles", "<i8")])
         for k, v in enumerate(variants):
             if v is None:
                 fits.append(INVALID_FITNESS)
