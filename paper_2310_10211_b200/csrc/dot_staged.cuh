@@ -937,25 +937,27 @@ __device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, d
     const bool act0 = !SCALAR && rb * 8 < pm && cb0 * 8 < ncols;
     const bool act1 = !ACC8 && act0 && (cb0 + 1) * 8 < ncols;
     if (SCALAR) {
+      // the thread's 4 outputs (rows mm + 8u, column nn) advance together so
+      // their 4 dependent chains overlap; invalid rows compute garbage that is
+      // never stored
+      const int mm = threadIdx.x >> 5, nn = threadIdx.x & 31;
+      const double* pa = As + mm * ars;
+      const double* pb = Bs + nn * brs;
+      const int ra = 8 * ars;
+      if (CK == 2) {
+#pragma unroll 4
+        for (int kk = 0; kk < nk; ++kk) {
+          const double b = pb[kk * bks];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int o = threadIdx.x + u * kDotThreads;
-        const int mm = o >> 5, nn = o & 31;
-        if (mm < pm && nn < ncols) {
-          const double* pa = As + mm * ars;
-          const double* pb = Bs + nn * brs;
-          double v = acc[u];
-          if (CK == 2) {
+          for (int u = 0; u < 4; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(pa[u * ra + kk * aks], b));
+        }
+      } else {
 #pragma unroll 4
-            for (int kk = 0; kk < nk; ++kk) v = __dadd_rn(v, __dmul_rn(pa[kk * aks], pb[kk * bks]));
-          } else {
-            uint64_t w = (uint64_t)as_i64(v);
-#pragma unroll 4
-            for (int kk = 0; kk < nk; ++kk)
-              w += (uint64_t)as_i64(pa[kk * aks]) * (uint64_t)as_i64(pb[kk * bks]);
-            v = as_w((int64_t)w);
-          }
-          acc[u] = v;
+        for (int kk = 0; kk < nk; ++kk) {
+          const uint64_t b = (uint64_t)as_i64(pb[kk * bks]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            acc[u] = as_w((int64_t)((uint64_t)as_i64(acc[u]) + (uint64_t)as_i64(pa[u * ra + kk * aks]) * b));
         }
       }
     }
