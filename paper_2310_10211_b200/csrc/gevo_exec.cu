@@ -154,21 +154,55 @@ __device__ __noinline__ void ew_instr(const Shared& S, const gevo_instr& I, F f)
     }
     return;
   }
-  for (int i = threadIdx.x; i < n; i += kThreads) {
-    int idx[GEVO_MAXR];
-    unravel(i, rank, I.shp, idx);
-    int64_t ad[4];
+  // rank 3..6: the thread's multi-index advances by kThreads in the shape's
+  // mixed radix (digit add with carry) -- no division per element
+  int idx[GEVO_MAXR], dig[GEVO_MAXR], shp[GEVO_MAXR], st[4][GEVO_MAXR];
+  unravel(threadIdx.x, rank, I.shp, idx);
+  unravel(kThreads, rank, I.shp, dig);
+  // strides and shape into registers: stores through `out` may alias the
+  // (shared-memory) instruction record, which would force reloads
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int64_t v = off[k];
-      if (k <= NIN)
-        for (int d = 0; d < rank; ++d) v += (int64_t)idx[d] * ops[k]->st[d];
-      ad[k] = v;
+  for (int d = 0; d < GEVO_MAXR; ++d) {
+    shp[d] = I.shp[d];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) st[k][d] = k <= NIN ? ops[k]->st[d] : 0;
+  }
+  constexpr int U = 4;
+  for (int base = threadIdx.x; base < n; base += U * kThreads) {
+    int ao[U];
+    double a[U], b[U], c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (base + u * kThreads < n) {
+        int ad[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          int v = off[k];
+          if (k <= NIN) {
+#pragma unroll
+            for (int d = 0; d < GEVO_MAXR; ++d)
+              if (d < rank) v += idx[d] * st[k][d];
+          }
+          ad[k] = v;
+        }
+        ao[u] = ad[0];
+        a[u] = in0[ad[1]];
+        if (NIN > 1) b[u] = in1[ad[2]];
+        if (NIN > 2) c[u] = in2[ad[3]];
+      }
+      int carry = 0;
+#pragma unroll
+      for (int d = GEVO_MAXR - 1; d >= 0; --d) {
+        if (d < rank) {
+          int v = idx[d] + dig[d] + carry;
+          carry = v >= shp[d];
+          idx[d] = carry ? v - shp[d] : v;
+        }
+      }
     }
-    const double a = in0[ad[1]];
-    const double b = NIN > 1 ? in1[ad[2]] : 0.0;
-    const double c = NIN > 2 ? in2[ad[3]] : 0.0;
-    out[ad[0]] = f(a, b, c);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (base + u * kThreads < n) out[ao[u]] = f(a[u], NIN > 1 ? b[u] : 0.0, NIN > 2 ? c[u] : 0.0);
   }
 }
 
@@ -219,38 +253,76 @@ __device__ __noinline__ void run_pad(const Shared& S, const gevo_instr& I) {
     }
     return;
   }
-  for (int i = threadIdx.x; i < I.n; i += kThreads) {
-    int idx[GEVO_MAXR];
-    unravel(i, I.rank, I.shp, idx);
+  int idx[GEVO_MAXR], dig[GEVO_MAXR], shp[GEVO_MAXR], lo[GEVO_MAXR], ex[GEVO_MAXR], is[GEVO_MAXR],
+      os[GEVO_MAXR];
+  const int rank = I.rank, n = I.n, ioff = I.in[0].off, ooff = I.out.off;
+  unravel(threadIdx.x, rank, I.shp, idx);
+  unravel(kThreads, rank, I.shp, dig);
+#pragma unroll
+  for (int d = 0; d < GEVO_MAXR; ++d) {   // registers (stores may alias the record)
+    shp[d] = I.shp[d];
+    lo[d] = I.aux[d];
+    ex[d] = I.aux2[d];
+    is[d] = I.in[0].st[d];
+    os[d] = I.out.st[d];
+  }
+  for (int i = threadIdx.x; i < n; i += kThreads) {
     bool inside = true;
-    int64_t src = I.in[0].off;
+    int src = ioff, dst = ooff;
 #pragma unroll
     for (int d = 0; d < GEVO_MAXR; ++d) {
-      if (d < I.rank) {
-        int j = idx[d] - I.aux[d];
-        inside = inside && j >= 0 && j < I.aux2[d];
-        src += (int64_t)j * I.in[0].st[d];
+      if (d < rank) {
+        const int j = idx[d] - lo[d];
+        inside = inside && j >= 0 && j < ex[d];
+        src += j * is[d];
+        dst += idx[d] * os[d];
       }
     }
-    out[addr(I.out, idx, I.rank)] = inside ? in[src] : pv;
+    out[dst] = inside ? in[src] : pv;
+    int carry = 0;
+#pragma unroll
+    for (int d = GEVO_MAXR - 1; d >= 0; --d) {
+      if (d < rank) {
+        int v = idx[d] + dig[d] + carry;
+        carry = v >= shp[d];
+        idx[d] = carry ? v - shp[d] : v;
+      }
+    }
   }
 }
 
 __device__ __noinline__ void run_reduce(const Shared& S, const gevo_instr& I) {
   double* out = opptr(S, I.out);
   const double* in = opptr(S, I.in[0]);
-  const int L = I.aux[0];
+  // the record's fields into registers (stores may alias it)
+  const int L = I.aux[0], n = I.n, rank = I.rank, kin = I.kin, sub = I.sub;
   const int64_t rs = I.aux[1];
-  for (int i = threadIdx.x; i < I.n; i += blockDim.x) {
+  int shp[GEVO_MAXR], ist[GEVO_MAXR], ost[GEVO_MAXR];
+#pragma unroll
+  for (int d = 0; d < GEVO_MAXR; ++d) {
+    shp[d] = I.shp[d];
+    ist[d] = I.in[0].st[d];
+    ost[d] = I.out.st[d];
+  }
+  const int ioff = I.in[0].off, ooff = I.out.off;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
     int idx[GEVO_MAXR];
-    unravel(i, I.rank, I.shp, idx);
-    const double* p = in + addr(I.in[0], idx, I.rank);
+    unravel(i, rank, shp, idx);
+    int src = ioff, dst = ooff;
+#pragma unroll
+    for (int d = 0; d < GEVO_MAXR; ++d) {
+      if (d < rank) {
+        src += idx[d] * ist[d];
+        dst += idx[d] * ost[d];
+      }
+    }
+    const double* p = in + src;
     double r;
-    if (I.kin == GEVO_K_F64) {
-      if (I.sub == GEVO_R_MAX) {
+    if (kin == GEVO_K_F64) {
+      if (sub == GEVO_R_MAX) {
         r = p[0];
         for (int k = 1; k < L; ++k) r = np_fmax(r, p[k * rs]);
-      } else if (I.sub == GEVO_R_SUM_PAIRWISE) {
+      } else if (sub == GEVO_R_SUM_PAIRWISE) {
         r = pairwise_sum(p, L, rs);
       } else {
         r = 0.0;
@@ -258,7 +330,7 @@ __device__ __noinline__ void run_reduce(const Shared& S, const gevo_instr& I) {
       }
     } else {
       int64_t v;
-      if (I.sub == GEVO_R_MAX) {
+      if (sub == GEVO_R_MAX) {
         v = as_i64(p[0]);
         for (int k = 1; k < L; ++k) { int64_t x = as_i64(p[k * rs]); v = x > v ? x : v; }
       } else {
@@ -268,7 +340,7 @@ __device__ __noinline__ void run_reduce(const Shared& S, const gevo_instr& I) {
       }
       r = as_w(v);
     }
-    out[addr(I.out, idx, I.rank)] = r;
+    out[dst] = r;
   }
 }
 

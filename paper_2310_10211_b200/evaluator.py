@@ -113,8 +113,11 @@ class DeviceEvaluator:
                               cfg.classes, cfg.batch_size)
         self.n_search_batches = len(ds.search.labels) // cfg.batch_size
         self._holdout_batches = None
+        # weight arrays in parameter order (w1, b1, w2, b2 for 2fcNet; the
+        # flat vector w for the CNN)
+        self.weight_names = list(workload.weights)
         w = [np.ascontiguousarray(workload.weights[n], dtype=np.float64)
-             for n in WEIGHT_NAMES]
+             for n in self.weight_names]
         self.weight_shapes = [a.shape for a in w]
         self.ctx.upload_weights(np.concatenate([a.reshape(-1) for a in w]))
         self.weight_elems = int(sum(a.size for a in w))
@@ -247,7 +250,7 @@ class DeviceEvaluator:
 
     def split_weights(self, flat):
         out, o = {}, 0
-        for name, shape in zip(WEIGHT_NAMES, self.weight_shapes):
+        for name, shape in zip(self.weight_names, self.weight_shapes):
             n = int(np.prod(shape))
             out[name] = np.array(flat[o:o + n]).reshape(shape)
             o += n

@@ -1,0 +1,117 @@
+"""CNN prediction fixtures from the REAL reference (build container only).
+
+    PYTHONPATH=/root/reference/pkg/src:. PYTHONDONTWRITEBYTECODE=1 \
+    python tests/golden/make_cnn_golden.py
+
+The CNN workload is new, so its oracle is the
+reference's own interpreter and mutation engine run on the network text:
+
+  * the module text of paper_2310_10211_b200.cnn is parsed by the reference
+    parser (parser.py:337) -- the dialect is unchanged;
+  * mutants come from the reference's genome.mutate (genome.py:626-657),
+    chained like search._mutated (search.py:283-293), with the reference's
+    smoke rule (fitness.py:82-96: one forward run on batch 0);
+  * each variant is scored with the reference interpreter (interpreter.py:
+    188-225) over the search batches exactly like _misclassification
+    (fitness.py:355-369), and its static cost is the reference's
+    (interpreter.py:41-59, fitness.py:387-388).
+
+Writes tests/golden/cnn_pop.json.gz.
+"""
+from __future__ import annotations
+
+import gzip
+import json
+import os
+import random
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from evotir.genome import MutationError, apply_patch, mutate, patch_dumps  # noqa: E402
+from evotir.interpreter import get_plan  # noqa: E402
+from evotir.ir import Module  # noqa: E402
+from evotir.parser import parse_module  # noqa: E402
+from evotir.printer import print_module  # noqa: E402
+
+from paper_2310_10211_b200 import cnn  # noqa: E402
+
+N_VARIANTS = 16
+MAX_EDITS = 3
+
+
+def fn_text(fn) -> str:
+    return print_module(Module(functions={fn.name: fn}, constants={}))
+
+
+def main():
+    cfg = cnn.CnnConfig(search_n=30, holdout_n=10)
+    wl = cnn.build_cnn_prediction_workload(cfg)
+    text, flat = cnn.cnn_forward_text(cfg)
+    module = parse_module(text)
+    B, S, C = cfg.batch_size, cfg.side, cfg.in_channels
+    xs = wl.search_x.reshape(-1, B, S, S, C)
+    lbs = wl.search_labels
+
+    def probs_of(mod, xb):
+        plan = get_plan(mod.functions["forward"])
+        with np.errstate(all="ignore"):
+            return plan.run([flat, xb])[0]
+
+    def smoke(mod):
+        try:
+            probs_of(mod, xs[0])
+            return True
+        except Exception:
+            return False
+
+    def score(mod):
+        plan = get_plan(mod.functions["forward"])
+        wrong = total = 0
+        for xb, lb in zip(xs, lbs):
+            with np.errstate(all="ignore"):
+                (p,) = plan.run([flat, xb])
+            if not np.all(np.isfinite(p)):
+                return dict(wrong=0, total=0, status=2, error=1.0, cost=plan.total_cost * len(xs))
+            wrong += int(np.sum(np.argmax(p, axis=1) != lb))
+            total += len(lb)
+        return dict(wrong=wrong, total=total, status=0, error=wrong / total,
+                    cost=plan.total_cost * len(xs))
+
+    rng = random.Random(2310)
+    inds = []
+    patch = ()
+    variants = [()]
+    while len(variants) < N_VARIANTS:
+        base = variants[rng.randrange(len(variants))] if len(variants) > 1 else ()
+        if len(base) >= MAX_EDITS:
+            base = ()
+        variant = apply_patch(module, base).module
+        try:
+            edit = mutate(variant, rng, functions=["forward"], smoke=smoke)
+        except MutationError:
+            continue
+        variants.append(base + (edit,))
+    for patch in variants:
+        mod = apply_patch(module, patch).module
+        rec = score(mod)
+        rec.update(key=patch_dumps(patch), edits=len(patch),
+                   forward=fn_text(mod.functions["forward"]))
+        inds.append(rec)
+        print(f"edits {len(patch)}: cost {rec['cost']:.0f} wrong {rec['wrong']}/{rec['total']} "
+              f"status {rec['status']}")
+    out = {"config": {"search_n": cfg.search_n, "holdout_n": cfg.holdout_n,
+                      "batch_size": cfg.batch_size},
+           "individuals": inds}
+    path = os.path.join(HERE, "cnn_pop.json.gz")
+    with gzip.open(path, "wt") as f:
+        json.dump(out, f, separators=(",", ":"), sort_keys=True)
+    print(f"wrote {path} ({os.path.getsize(path)} bytes)")
+
+
+if __name__ == "__main__":
+    main()
