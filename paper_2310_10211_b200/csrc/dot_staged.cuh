@@ -1075,6 +1075,139 @@ __device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, d
   cp_async_wait<0>();
 }
 
+
+// ---------------------------------------------------------------------------
+// Tiny dots (M, N, K <= 32: the hidden/output-layer dots of the MLP step):
+// no staging -- each lane reads its DMMA fragments straight from the
+// operands (shared-memory arena or global) and applies the epilogue to its
+// own outputs.  FMA: warp = 8x16 strip (two tiles); ACC8: warp = one 8x8
+// tile with its 8 lane chains.
+template <bool ACC8, int EK>
+__device__ __noinline__ void dot_tiny(const DotArgs& dref, int col0, int col1, const EpiDev* epi,
+                                      const EpiR& R, int mode) {
+  const DotArgs d = dref;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int M = d.M, K = d.K, ncols = col1 - col0;
+  const int rb = warp >> 1, cb0 = ACC8 ? (warp & 1) : (warp & 1) * 2;
+  if (rb * 8 >= M || cb0 * 8 >= ncols) return;
+  const int ntile = ACC8 ? 1 : ((cb0 + 1) * 8 < ncols ? 2 : 1);
+  const int m = rb * 8 + g;
+  const int mc = min(m, M - 1);                        // clamped (valid) row for loads
+  double acc[ACC8 ? 16 : 4];
+#pragma unroll
+  for (int i = 0; i < (ACC8 ? 16 : 4); ++i) acc[i] = 0.0;
+  const double* arow = d.A + (int64_t)mc * d.sam;
+  int bcol[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) bcol[t] = col0 + min((cb0 + t) * 8 + g, ncols - 1);
+  if (!ACC8) {
+    const int nq = K >> 2;
+#pragma unroll 8
+    for (int q = 0; q < nq; ++q) {
+      const int k = 4 * q + t4;
+      const double a = arow[(int64_t)k * d.sak];
+      dmma884(acc[0], acc[1], a, d.B[(int64_t)k * d.sbk + (int64_t)bcol[0] * d.sbn]);
+      if (ntile > 1) dmma884(acc[2], acc[3], a, d.B[(int64_t)k * d.sbk + (int64_t)bcol[1] * d.sbn]);
+    }
+    for (int k = nq * 4; k < K; ++k) {                 // k tail: scalar fma chain
+      const double a = arow[(int64_t)k * d.sak];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int nn = (h >> 1) * 8 + 2 * t4 + (h & 1);
+        if ((h < 2 || ntile > 1) && cb0 * 8 + nn < ncols)
+          acc[h] = fma(a, d.B[(int64_t)k * d.sbk + (int64_t)(col0 + cb0 * 8 + nn) * d.sbn], acc[h]);
+      }
+    }
+  } else {
+    const int kmain = mode == GEVO_D_ACC8_TAIL ? (K & ~7) : K;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      for (int k0 = 0; k0 < kmain; k0 += 32) {
+        if (k0 + j + 24 < kmain) {
+          const int k = k0 + j + 8 * t4;
+          dmma884(acc[2 * j], acc[2 * j + 1], arow[(int64_t)k * d.sak],
+                  d.B[(int64_t)k * d.sbk + (int64_t)bcol[0] * d.sbn]);
+        } else {
+          for (int t = 0; t < 4; ++t) {
+            const int k = k0 + j + 8 * t;
+            if (k >= kmain) break;
+            const double a = arow[(int64_t)k * d.sak];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int nn = cb0 * 8 + 2 * t4 + h;
+              if (nn < ncols)
+                acc[2 * j + h] = fma(a, d.B[(int64_t)k * d.sbk + (int64_t)(col0 + nn) * d.sbn], acc[2 * j + h]);
+            }
+          }
+        }
+      }
+    }
+    double r[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      r[h] = __dadd_rn(__dadd_rn(__dadd_rn(acc[h], acc[2 + h]), __dadd_rn(acc[4 + h], acc[6 + h])),
+                       __dadd_rn(__dadd_rn(acc[8 + h], acc[10 + h]), __dadd_rn(acc[12 + h], acc[14 + h])));
+      const int nn = cb0 * 8 + 2 * t4 + h;
+      for (int k = kmain; k < K; ++k)                  // ACC8_TAIL
+        if (nn < ncols)
+          r[h] = fma(arow[(int64_t)k * d.sak], d.B[(int64_t)k * d.sbk + (int64_t)(col0 + nn) * d.sbn], r[h]);
+    }
+    acc[0] = r[0];
+    acc[1] = r[1];
+  }
+  if (m >= M) return;
+  double* orow = d.out + (int64_t)m * d.som;
+#pragma unroll
+  for (int h = 0; h < (ACC8 ? 2 : 4); ++h) {
+    const int nn = cb0 * 8 + (h >> 1) * 8 + 2 * t4 + (h & 1);
+    if ((h < 2 || ntile > 1) && nn < ncols) {
+      const int n = col0 + nn;
+      double v = acc[h];
+      if (EK == EK_CHAIN) {
+#pragma unroll
+        for (int x = 0; x < kEpiPre; ++x) {
+          if (x < R.nops) {
+            const double o = R.src[x] == ES_SCALAR ? R.sval[x]
+                                                   : R.ptr[x][(int64_t)m * R.st0[x] + (int64_t)n * R.st1[x]];
+            v = R.fleft[x] ? bin_f64(R.fsub[x], v, o) : bin_f64(R.fsub[x], o, v);
+          }
+        }
+      } else if (EK == EK_SELECT) {
+        const double o0 = R.src[0] == ES_SCALAR ? R.sval[0]
+                                                : R.ptr[0][(int64_t)m * R.st0[0] + (int64_t)n * R.st1[0]];
+        const double o1 = R.src[1] == ES_SCALAR ? R.sval[1]
+                                                : R.ptr[1][(int64_t)m * R.st0[1] + (int64_t)n * R.st1[1]];
+        const bool p = as_i64(o0) != 0;
+        v = R.fleft[0] ? (p ? v : o1) : (p ? o1 : v);
+      } else if (EK == EK_GENERIC) {
+        double ev[kEpiPre];
+        epi_fetch(*epi, m, n, ev);
+        v = epilogue_generic(*epi, ev, v, m, n);
+      }
+      orow[(int64_t)n * d.son] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ void dot_tiny_dispatch(const DotArgs& d, int col0, int col1, const EpiDev* epi,
+                                                  bool acc8, int mode) {
+  __shared__ EpiR R;
+  const int ek = !epi ? EK_NONE : (epi->fast == 1 ? EK_CHAIN : (epi->fast == 2 ? EK_SELECT : EK_GENERIC));
+  if (threadIdx.x == 0) epi_init(R, ek == EK_CHAIN || ek == EK_SELECT ? epi : nullptr, false);
+  __syncthreads();
+#define GEVO_TINY(A8)                                                         \
+  switch (ek) {                                                               \
+    case EK_NONE: dot_tiny<A8, EK_NONE>(d, col0, col1, epi, R, mode); break;  \
+    case EK_CHAIN: dot_tiny<A8, EK_CHAIN>(d, col0, col1, epi, R, mode); break; \
+    case EK_SELECT: dot_tiny<A8, EK_SELECT>(d, col0, col1, epi, R, mode); break; \
+    default: dot_tiny<A8, EK_GENERIC>(d, col0, col1, epi, R, mode); break;     \
+  }
+  if (acc8) { GEVO_TINY(true) } else { GEVO_TINY(false) }
+#undef GEVO_TINY
+  __syncthreads();
+}
+
 // PANELS needs its tile-staged epilogue operand (the first full-matrix one,
 // see epi_init) to be made of whole aligned lines
 __device__ __forceinline__ bool dot_etile_ok(const EpiDev* e, int ncols, int M) {
@@ -1094,6 +1227,10 @@ __device__ __forceinline__ void dot_columns(const DotArgs& d, int col0, int col1
   // pipeline otherwise
   const int ck = integer ? 3 : (mode == GEVO_D_SEQ_NOFMA ? 2 : (mode == GEVO_D_FMA_CHAIN ? 0 : 1));
   const int width = ck == 1 ? 16 : kPanel;
+  if (ck <= 1 && d.M <= kPanel && d.K <= kKC && col1 - col0 <= (ck == 1 ? 16 : kPanel)) {
+    dot_tiny_dispatch(d, col0, col1, epi, ck == 1, mode);
+    return;
+  }
   const bool kstream = d.M <= kPanel && d.K > kKC;
   const bool panels = d.K <= kKC && (!epi || epi->fast == 0 || dot_etile_ok(epi, col1 - col0, d.M));
   if (kstream || panels) {
