@@ -11,6 +11,7 @@
 // reference may return a parameter unchanged, genome.py:471-478).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <mutex>
 #include "gevo_plan.h"
 #include "exec_core.cuh"
 #include "exp_np.cuh"
@@ -683,15 +684,33 @@ exec_once_kernel(OnceArgs args) {
   run_instrs(S, ins, P.train0_n, dstage, nullptr);
 }
 
+// The dynamic shared-memory ceiling is a per-function attribute shared by
+// every context (and host thread) of the process: raise it once to the
+// opt-in maximum instead of per launch, so two contexts launching
+// concurrently with different plan sizes cannot lower it under each other.
+template <class K>
+static void raise_smem_ceiling(K kernel) {
+  static std::once_flag once[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::call_once(once[dev & 63], [&] {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, kernel);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  });
+}
+
 void launch_eval(const EvalArgs& a, int n_prog, cudaStream_t st) {
   const size_t smem = (size_t)(a.smem_elems + kStageElems) * sizeof(double);
-  cudaFuncSetAttribute(eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  raise_smem_ceiling(eval_kernel);
   eval_kernel<<<n_prog, kThreads, smem, st>>>(a);
 }
 
 void launch_once(const OnceArgs& a, int n_prog, cudaStream_t st) {
   const size_t smem = (size_t)(a.smem_elems + kStageElems) * sizeof(double);
-  cudaFuncSetAttribute(exec_once_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  raise_smem_ceiling(exec_once_kernel);
   exec_once_kernel<<<n_prog, kThreads, smem, st>>>(a);
 }
 
