@@ -260,19 +260,26 @@ def main():
     clocks = Clocks(local)
     # (1) value: plans built before timing; one launch per step on one
     # context; device time of the evaluation kernel (CUDA events)
-    plans = []
+    lowered_steps = []
     for s in range(total_steps):
-        vps = [v for v in lower_all(batches[s][1], wl.config.cost_table, True) if v is not None]
-        plans.append(build_population_plan(vps, ev.weight_shapes, ev.batch * ev.classes))
+        lowered_steps.append([v for v in lower_all(batches[s][1], wl.config.cost_table, True)
+                              if v is not None])
+    from paper_2310_10211_b200.plan import device_weight, layout_order, sm_aware_order
     for s in range(total_steps):
         sel, fns = batches[s]
+        vps = lowered_steps[s]
+        # launch order from the block -> SM layout the previous launch showed
+        wts = [device_weight(v, steps_cfg, nb) for v in vps]
+        layout = ev._sm_layout.get(len(vps))
+        order = layout_order(wts, layout) if layout else sm_aware_order(wts, ev.n_sms)
+        p = build_population_plan(vps, ev.weight_shapes, ev.batch * ev.classes, order=order)
         flush.zero_()                       # L2 flush between iterations
         barrier()
         if s == args.warmup:
             clocks.start()
-        p = plans[s]
-        ev.ctx.eval(p.blob, p.n_prog, 0, steps_cfg, wl.config.finite_check_every, 0, 0,
-                    ev.weight_elems, False)
+        res, _ = ev.ctx.eval(p.blob, p.n_prog, 0, steps_cfg, wl.config.finite_check_every, 0, 0,
+                             ev.weight_elems, False)
+        ev._learn_layout(res, order)
         if s >= args.warmup:
             kern_ms.append(ev.ctx.last_kernel_ms())
             alg_bytes.append(sum(per_individual_bytes(f, steps_cfg, nb) for f in fns))

@@ -76,6 +76,9 @@ typedef struct {
   int32_t steps_run;  /* training steps executed before an early exit */
   int64_t cycles;     /* SM clock cycles this individual's CTA ran (diagnostics:
                          load balance, stragglers) */
+  int64_t t0_ns, t1_ns; /* global timer at the CTA's start and end (ns) */
+  int32_t smid;       /* SM the CTA ran on */
+  int32_t pad;
 } gevo_result;
 
 typedef struct {

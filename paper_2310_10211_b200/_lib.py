@@ -22,12 +22,14 @@ c_i64p = ctypes.POINTER(ctypes.c_int64)
 class GevoResult(ctypes.Structure):
     _fields_ = [("wrong", ctypes.c_int64), ("total", ctypes.c_int64),
                 ("status", ctypes.c_int32), ("steps_run", ctypes.c_int32),
-                ("cycles", ctypes.c_int64)]
+                ("cycles", ctypes.c_int64), ("t0_ns", ctypes.c_int64),
+                ("t1_ns", ctypes.c_int64), ("smid", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 RESULT_DTYPE = np.dtype([("wrong", "<i8"), ("total", "<i8"),
                          ("status", "<i4"), ("steps_run", "<i4"),
-                         ("cycles", "<i8")])
+                         ("cycles", "<i8"), ("t0_ns", "<i8"), ("t1_ns", "<i8"),
+                         ("smid", "<i4"), ("pad", "<i4")])
 
 
 class GevoEvalDesc(ctypes.Structure):
@@ -131,6 +133,12 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    def num_sms(self) -> int:
+        """SM count of the context's device (from gevo_device_info)."""
+        import re
+        m = re.search(r"(\d+) SMs", self.device_info())
+        return int(m.group(1)) if m else 148
 
     def device_info(self) -> str:
         buf = ctypes.create_string_buffer(256)

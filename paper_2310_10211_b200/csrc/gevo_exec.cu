@@ -576,6 +576,8 @@ eval_kernel(EvalArgs args) {
   int status = GEVO_STATUS_OK;
   int steps_run = 0;
   const long long t_start = clock64();
+  unsigned long long g_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
 
   const double* final_w = args.init_weights;
   if (args.mode == GEVO_MODE_TRAIN && args.steps > 0) {
@@ -654,6 +656,13 @@ eval_kernel(EvalArgs args) {
     R->status = status;
     R->steps_run = steps_run;
     R->cycles = clock64() - t_start;
+    unsigned long long g_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+    R->t0_ns = (int64_t)g_start;
+    R->t1_ns = (int64_t)g_end;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    R->smid = (int32_t)smid;
   }
   if (args.final_weights != nullptr) {
     double* dst = args.final_weights + (int64_t)P.result_slot * args.weight_elems;

@@ -19,7 +19,8 @@ import time
 import numpy as np
 
 from . import _lib
-from .plan import build_population_plan, lower_variant
+from .plan import (build_population_plan, device_weight, layout_order, lower_variant,
+                   sm_aware_order)
 from .workloads import (INVALID_FITNESS, PREDICTION, TRAINING, WEIGHT_NAMES,
                         Fitness, Workload)
 
@@ -106,6 +107,7 @@ class DeviceEvaluator:
         self.workload = workload
         self.device = device
         self.ctx = _lib.Context(device)
+        self.n_sms = self.ctx.num_sms()
         cfg = workload.config
         self.batch, self.classes = cfg.batch_size, cfg.classes
         ds = workload.dataset
@@ -123,9 +125,19 @@ class DeviceEvaluator:
         self.weight_elems = int(sum(a.size for a in w))
         self._flat_weights = np.concatenate([a.reshape(-1) for a in w])
         self._ctx2 = None
+        self._sm_layout = {}
         self.last_timing = {}
         self.last_plan_bytes = 0
         self.last_device_ms = 0.0
+
+    def _learn_layout(self, res, order):
+        """Remember which launch slots shared an SM (records carry the SM id
+        of every CTA) for the next launch of the same size."""
+        sm = res["smid"][np.asarray(order)]
+        groups = {}
+        for block, s in enumerate(sm.tolist()):
+            groups.setdefault(s, []).append(block)
+        self._sm_layout[len(order)] = list(groups.values())
 
     def _second_context(self):
         """A second context (own stream and buffers) on the same device: the
@@ -201,7 +213,11 @@ class DeviceEvaluator:
                     slots.append(i)
             if not lowered:
                 continue
-            plan = build_population_plan(lowered, self.weight_shapes, self.batch * self.classes)
+            wts = [device_weight(v, cfg.steps if training else 0, n_score) for v in lowered]
+            layout = self._sm_layout.get(len(lowered))
+            order = layout_order(wts, layout) if layout else sm_aware_order(wts, self.n_sms)
+            plan = build_population_plan(lowered, self.weight_shapes, self.batch * self.classes,
+                                         order=order)
             tc = time.perf_counter()
             t_lower += tb - ta
             t_pack += tc - tb
@@ -209,8 +225,8 @@ class DeviceEvaluator:
             args = (plan.blob, plan.n_prog, 0 if training else 1, cfg.steps if training else 0,
                     cfg.finite_check_every, SPLIT_SEARCH, split, self.weight_elems, want_weights)
 
-            def run(c=ctxs[h], a=args, key=h, lv=lowered, sl=slots):
-                box[key] = (c.eval(*a), lv, sl)
+            def run(c=ctxs[h], a=args, key=h, lv=lowered, sl=slots, od=order):
+                box[key] = (c.eval(*a), lv, sl, od)
             if h + 1 < len(jobs):
                 import threading
                 runner = threading.Thread(target=run)
@@ -225,7 +241,8 @@ class DeviceEvaluator:
         elif used:
             self.last_device_ms = ctxs[used[0]].last_kernel_ms()
         for key in used:
-            (res, fw), lowered, slots = box[key]
+            (res, fw), lowered, slots, order = box[key]
+            self._learn_layout(res, order)
             for k, vp in enumerate(lowered):
                 i = slots[k]
                 r = res[k]

@@ -102,6 +102,88 @@ def _encode_shifted(low, pool):
     return arr
 
 
+OP_DOT = 5
+# relative device cost of a MAC per summation order (measured on B200 with
+# tests/tools/stragglers.py: FMA chain on DMMA; ACC8 runs its 8 chains in
+# 16-column passes; numpy's no-FMA loop and integer dots are scalar)
+_MODE_WEIGHT = {0: 1.0, 1: 2.0, 3: 2.0, 2: 3.0}
+
+
+def device_weight(v: VariantPlan, steps: int = 600, batches: int = 31) -> float:
+    """Estimated device time of one individual: dot MACs weighted by the
+    kernel path their summation order takes, plus element counts of the other
+    instructions, over the train and scoring invocations."""
+    def fn_weight(arr):
+        if arr is None:
+            return 0.0
+        w = 0.0
+        for r in arr:
+            op = int(r["op"])
+            if op == OP_DOT:
+                m, n, k = int(r["shp"][0]), int(r["shp"][1]), int(r["aux"][0])
+                split = min(int(r["aux"][1]), n)
+                w += m * k * (split * _MODE_WEIGHT.get(int(r["sub"]), 3.0)
+                              + (n - split) * _MODE_WEIGHT.get(int(r["aux"][2]), 3.0))
+                w += 20000.0
+            elif op != 7:
+                w += 4.0 * int(r["n"]) + 4000.0
+        return w
+    return steps * fn_weight(v.train1) + batches * fn_weight(v.fwd)
+
+
+def sm_aware_order(weights, n_sms: int):
+    """Launch order for a one-wave launch of n <= 2 * n_sms CTAs.  Blocks are
+    dealt to SMs in index order, so blocks n - n_sms .. n_sms - 1 get an SM to
+    themselves while block i < n - n_sms shares one with block n_sms + i.  The
+    heaviest individuals take the solo SMs; the rest pair heaviest with
+    lightest, so the slowest CTA -- the launch time -- is as short as it can
+    be.  Falls back to heaviest-first outside one wave."""
+    w = np.asarray(weights, dtype=np.float64)
+    n = len(w)
+    by = list(np.argsort(-w, kind="stable"))
+    if n <= n_sms or n > 2 * n_sms:
+        return np.asarray(by)
+    pairs = n - n_sms                       # SMs hosting two blocks
+    solo = n_sms - pairs
+    order = np.zeros(n, dtype=np.int64)
+    order[pairs:n_sms] = by[:solo]          # heaviest run alone
+    rest = by[solo:]                        # 2 * pairs individuals, heaviest first
+    for i in range(pairs):
+        order[i] = rest[i]                  # heavy ...
+        order[n_sms + i] = rest[-1 - i]     # ... paired with light
+    return order
+
+
+def layout_order(weights, groups):
+    """Launch order from an observed block -> SM layout: `groups` lists the
+    block ids that shared an SM in an earlier launch of the same size.
+    Heaviest individuals go to the blocks that had an SM alone; the rest are
+    paired heaviest with lightest on the shared SMs."""
+    w = np.asarray(weights, dtype=np.float64)
+    by = list(np.argsort(-w, kind="stable"))
+    order = np.full(len(w), -1, dtype=np.int64)
+    alone = sorted(b for g in groups if len(g) == 1 for b in g)
+    shared = [g for g in groups if len(g) > 1]
+    k = 0
+    for b in alone:
+        order[b] = by[k]
+        k += 1
+    rest = by[k:]
+    lo, hi = 0, len(rest) - 1
+    for g in shared:
+        for j, b in enumerate(sorted(g)):
+            if lo > hi:
+                break
+            if j % 2 == 0:
+                order[b] = rest[lo]
+                lo += 1
+            else:
+                order[b] = rest[hi]
+                hi -= 1
+    assert (order >= 0).all() and len(set(order.tolist())) == len(w)
+    return order
+
+
 @dataclass
 class PopulationPlan:
     blob: np.ndarray          # uint8 bytes handed to gevo_eval

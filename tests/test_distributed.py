@@ -27,7 +27,9 @@ class TableBackend:
         fits = []
         recs = np.zeros(len(variants), dtype=[("wrong", "<i8"), ("total", "<i8"),
                                                ("status", "<i4"), ("steps_run", "<i4"),
-                                               ("cycles", "<i8")])
+                                               ("cycles", "<i8"), ("t0_ns", "<i8"),
+                                               ("t1_ns", "<i8"), ("smid", "<i4"),
+                                               ("pad", "<i4")])
         for k, v in enumerate(variants):
             if v is None:
                 fits.append(INVALID_FITNESS)

@@ -21,6 +21,9 @@ class FakeContext:
     def upload_split(self, *a):
         pass
 
+    def num_sms(self):
+        return 148
+
     def upload_weights(self, *a):
         pass
 
@@ -86,3 +89,18 @@ def test_pool_lowering_matches_in_process():
         assert x.train0.tobytes() == y.train0.tobytes()
         assert x.fwd.tobytes() == y.fwd.tobytes()
         assert x.consts.tobytes() == y.consts.tobytes()
+
+
+def test_sm_aware_order_places_heaviest_alone_and_pairs_heavy_with_light():
+    from paper_2310_10211_b200.plan import sm_aware_order
+    n_sms, n = 148, 256
+    w = np.arange(n, dtype=float)                     # individual i weighs i
+    order = sm_aware_order(w, n_sms)
+    assert sorted(order.tolist()) == list(range(n))   # a permutation
+    pairs = n - n_sms
+    solo = set(order[pairs:n_sms].tolist())
+    assert solo == set(range(n - (n_sms - pairs), n))  # the heaviest 40 run alone
+    sums = [w[order[i]] + w[order[n_sms + i]] for i in range(pairs)]
+    assert max(sums) - min(sums) <= 1.0               # heavy paired with light
+    # outside one wave: heaviest first
+    assert sm_aware_order(w[:100], n_sms).tolist() == list(range(99, -1, -1))

@@ -22,8 +22,31 @@ def main(start=0, n=256):
     fns = [{k: pf(i[k]) for k in ("forward", "train_step")} for i in sel]
     ev = DeviceEvaluator(W.build_2fcnet_workload())
     ev.evaluate_variants(fns[:8])
-    fits, rec = ev.evaluate_variants(fns, return_records=True)
+    from paper_2310_10211_b200.evaluator import lower_all
+    from paper_2310_10211_b200.plan import build_population_plan, device_weight, sm_aware_order
+    vps = lower_all(fns, None, True)
+    plan = build_population_plan(vps, ev.weight_shapes, 320,
+                                 order=sm_aware_order([device_weight(v) for v in vps], ev.n_sms))
+    rec, _ = ev.ctx.eval(plan.blob, plan.n_prog, 0, 600, 50, 0, 0, ev.weight_elems, False)
+    ev.last_device_ms = ev.ctx.last_kernel_ms()
     cyc = rec["cycles"].astype(np.float64)
+    t0, t1 = rec["t0_ns"], rec["t1_ns"]
+    base = t0.min()
+    print(f"CTA start spread {(t0.max() - base) / 1e6:.2f} ms, end spread {(t1.min() - base) / 1e6:.1f}.."
+          f"{(t1.max() - base) / 1e6:.1f} ms; SM clock from timers "
+          f"{np.median(cyc / np.maximum(t1 - t0, 1)):.3f} GHz")
+    cb = cyc[plan.order]                  # cycles by launch slot (block id)
+    sm = rec["smid"][plan.order]
+    shared = np.bincount(sm, minlength=int(sm.max()) + 1)[sm] > 1
+    print(f"CTAs alone on their SM: {int((~shared).sum())}; median cycles alone "
+          f"{np.median(cb[~shared]) if (~shared).any() else 0:.3g}, shared {np.median(cb[shared]):.3g}; "
+          f"blocks alone: {np.flatnonzero(~shared)[:8].tolist()}...")
+    nsm = ev.n_sms
+    if len(cb) > nsm:
+        pairs = len(cb) - nsm
+        print(f"by block: paired 0..{pairs - 1} median {np.median(cb[:pairs]):.3g}, "
+              f"solo {pairs}..{nsm - 1} median {np.median(cb[pairs:nsm]):.3g}, "
+              f"paired {nsm}.. median {np.median(cb[nsm:]):.3g}; max at block {int(np.argmax(cb))}")
     print(f"kernel span {ev.last_device_ms:.1f} ms; cycles per individual: "
           f"median {np.median(cyc):.3g}, p90 {np.percentile(cyc, 90):.3g}, max {cyc.max():.3g}")
     for i in np.argsort(-cyc)[:6]:
