@@ -37,7 +37,10 @@ def _lower_pool():
     GEVO_B200_LOWER_WORKERS=1 disables it."""
     global _POOL
     if _POOL is None:
-        n = int(os.environ.get("GEVO_B200_LOWER_WORKERS", min(16, os.cpu_count() or 1)))
+        # one share of the host's cores per local rank (torchrun sets
+        # LOCAL_WORLD_SIZE; every rank of a node lowers its own shard)
+        share = (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+        n = int(os.environ.get("GEVO_B200_LOWER_WORKERS", min(16, max(1, share))))
         if n <= 1:
             _POOL = False
         else:

@@ -40,11 +40,32 @@ def _E():
     return F, G, S
 
 
+_PICKLE_READY = False
+
+
+def _fast_pickling():
+    """Positional-tuple pickling for evotir's IR objects (same fields as this
+    package's dialect, see dialect.py): the evaluator ships variant functions
+    to its lowering processes and this is the part the parent pays serially."""
+    global _PICKLE_READY
+    if _PICKLE_READY:
+        return
+    import copyreg
+    import evotir.ir as IR
+    copyreg.pickle(IR.TensorType, lambda t: (IR.TensorType, (t.shape, t.kind)))
+    copyreg.pickle(IR.Operation, lambda o: (IR.Operation, (o.op_id, o.opcode, o.result,
+                                                           o.result_type, o.operands, o.attrs)))
+    copyreg.pickle(IR.FunctionBody, lambda f: (IR.FunctionBody, (f.name, f.params, f.ops,
+                                                                f.returns, f.return_types)))
+    _PICKLE_READY = True
+
+
 class _DeviceWorkload:
     """Adapter: an evotir Workload seen through the attributes
     DeviceEvaluator reads (config, dataset, weights, mode, module)."""
 
     def __init__(self, w):
+        _fast_pickling()
         self.source = w
         self.name = w.name
         self.mode = TRAINING if w.mode == "training" else PREDICTION
