@@ -695,6 +695,58 @@ __device__ __forceinline__ void feed_stage(Feed& f, const CopyPlan& cp, uint32_t
   }
 }
 
+
+// Fast epilogue on one lane's four DMMA outputs (row m; panel-local row mm;
+// columns nn, nn+1, nn+8, nn+9 of the piece starting at col0).  Operand
+// sources and op codes are warp-uniform: one dispatch per micro-op.
+__device__ __forceinline__ void epi_lane4(const EpiR& R, int ek, const double* Es, int ers, int eks,
+                                          double* v, int m, int col0, int mm, int nn, int ncols) {
+  if (ek == EK_NONE) return;
+  const int nx = ek == EK_SELECT ? 2 : R.nops;
+  double o[kEpiPre][4];
+#pragma unroll
+  for (int x = 0; x < kEpiPre; ++x) {
+    if (x < nx) {
+      const int src = R.src[x];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const int c = nn + (h >> 1) * 8 + (h & 1);
+        const bool in = c < ncols;
+        if (src == ES_SCALAR) o[x][h] = R.sval[x];
+        else if (src == ES_TILE) o[x][h] = in ? Es[mm * ers + c * eks] : 0.0;
+        else o[x][h] = in ? R.ptr[x][(int64_t)m * R.st0[x] + (int64_t)(col0 + c) * R.st1[x]] : 0.0;
+      }
+    }
+  }
+  if (ek == EK_SELECT) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const bool p = as_i64(o[0][h]) != 0;
+      v[h] = R.fleft[0] ? (p ? v[h] : o[1][h]) : (p ? o[1][h] : v[h]);
+    }
+    return;
+  }
+#pragma unroll
+  for (int x = 0; x < kEpiPre; ++x) {
+    if (x < nx) {
+      const bool left = R.fleft[x];
+#define GEVO_LANE_OP(EXPR)                                                  \
+  _Pragma("unroll") for (int h = 0; h < 4; ++h) {                           \
+    const double a = left ? v[h] : o[x][h], b = left ? o[x][h] : v[h];     \
+    v[h] = (EXPR);                                                          \
+  }
+      switch (R.fsub[x]) {
+        case GEVO_B_ADD: GEVO_LANE_OP(__dadd_rn(a, b)); break;
+        case GEVO_B_SUB: GEVO_LANE_OP(__dsub_rn(a, b)); break;
+        case GEVO_B_MUL: GEVO_LANE_OP(__dmul_rn(a, b)); break;
+        case GEVO_B_DIV: GEVO_LANE_OP(__ddiv_rn(a, b)); break;
+        default: GEVO_LANE_OP(np_fmax(a, b)); break;
+      }
+#undef GEVO_LANE_OP
+    }
+  }
+}
+
 // Lean variant of dot_fast for the hot case: FMA chain, every operand whole
 // aligned lines (VecCopy only; nothing else live across the loop).
 template <bool PANELS>
@@ -817,7 +869,27 @@ __device__ __noinline__ void dot_fast_vec(const DotArgs& dref, int col0, int col
     }
     GEVO_TSTAMP(tc)
     GEVO_TACC(3, tb, tc)
-    if (last) {
+    if (last && ek != EK_GENERIC) {
+      // epilogue on the accumulators: the lane holds row lm, columns ln, ln+1
+      // (tile 0) and ln+8, ln+9 (tile 1); one warp-uniform dispatch per
+      // micro-op for all four values
+      GEVO_TSTAMP(te0)
+      GEVO_TACC(4, tc, te0)
+      if (act0 && lm < pm) {
+        const int m = (PANELS ? s * kPanel : 0) + lm;
+        const double* Es = As + kTileElems;
+        epi_lane4(R, ek, Es, ers, eks, acc, m, col0, lm, ln, ncols);
+        double* orow = d.out + (int64_t)m * d.som + (int64_t)(col0 + ln) * d.son;
+        const int64_t s1 = d.son, s8 = 8 * d.son;
+        if (ln < ncols) orow[0] = acc[0];
+        if (ln + 1 < ncols) orow[s1] = acc[1];
+        if (act1 && ln + 8 < ncols) orow[s8] = acc[2];
+        if (act1 && ln + 9 < ncols) orow[s8 + s1] = acc[3];
+      }
+      acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+      GEVO_TSTAMP(te1)
+      GEVO_TACC(5, te0, te1)
+    } else if (last) {
       __syncthreads();                // A consumed: its region becomes the C tile
       double* Cs = As;
       if (act0) {
