@@ -699,22 +699,46 @@ __device__ __forceinline__ void feed_stage(Feed& f, const CopyPlan& cp, uint32_t
 // Fast epilogue on one lane's four DMMA outputs (row m; panel-local row mm;
 // columns nn, nn+1, nn+8, nn+9 of the piece starting at col0).  Operand
 // sources and op codes are warp-uniform: one dispatch per micro-op.
-__device__ __forceinline__ void epi_lane4(const EpiR& R, int ek, const double* Es, int ers, int eks,
+__device__ __forceinline__ void epi_lane4(const EpiR& Rs, int ek, const double* Es, int ers, int eks,
                                           double* v, int m, int col0, int mm, int nn, int ncols) {
   if (ek == EK_NONE) return;
-  const int nx = ek == EK_SELECT ? 2 : R.nops;
+  // the whole descriptor in registers first (independent shared loads),
+  // then uniform decisions
+  int nops = Rs.nops, src[kEpiPre], fsub[kEpiPre], fleft[kEpiPre], st0[kEpiPre], st1[kEpiPre];
+  double sval[kEpiPre];
+  const double* ptr[kEpiPre];
+#pragma unroll
+  for (int x = 0; x < kEpiPre; ++x) {
+    src[x] = Rs.src[x];
+    fsub[x] = Rs.fsub[x];
+    fleft[x] = Rs.fleft[x];
+    sval[x] = Rs.sval[x];
+    ptr[x] = Rs.ptr[x];
+    st0[x] = Rs.st0[x];
+    st1[x] = Rs.st1[x];
+  }
+  const int nx = ek == EK_SELECT ? 2 : nops;
   double o[kEpiPre][4];
 #pragma unroll
   for (int x = 0; x < kEpiPre; ++x) {
     if (x < nx) {
-      const int src = R.src[x];
+      if (src[x] == ES_SCALAR) {
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const int c = nn + (h >> 1) * 8 + (h & 1);
-        const bool in = c < ncols;
-        if (src == ES_SCALAR) o[x][h] = R.sval[x];
-        else if (src == ES_TILE) o[x][h] = in ? Es[mm * ers + c * eks] : 0.0;
-        else o[x][h] = in ? R.ptr[x][(int64_t)m * R.st0[x] + (int64_t)(col0 + c) * R.st1[x]] : 0.0;
+        for (int h = 0; h < 4; ++h) o[x][h] = sval[x];
+      } else if (src[x] == ES_TILE) {
+        const double* e = Es + mm * ers + nn * eks;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int c = (h >> 1) * 8 + (h & 1);
+          o[x][h] = nn + c < ncols ? e[c * eks] : 0.0;
+        }
+      } else {
+        const double* e = ptr[x] + (int64_t)m * st0[x] + (int64_t)(col0 + nn) * st1[x];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int c = (h >> 1) * 8 + (h & 1);
+          o[x][h] = nn + c < ncols ? e[(int64_t)c * st1[x]] : 0.0;
+        }
       }
     }
   }
@@ -722,20 +746,20 @@ __device__ __forceinline__ void epi_lane4(const EpiR& R, int ek, const double* E
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
       const bool p = as_i64(o[0][h]) != 0;
-      v[h] = R.fleft[0] ? (p ? v[h] : o[1][h]) : (p ? o[1][h] : v[h]);
+      v[h] = fleft[0] ? (p ? v[h] : o[1][h]) : (p ? o[1][h] : v[h]);
     }
     return;
   }
 #pragma unroll
   for (int x = 0; x < kEpiPre; ++x) {
     if (x < nx) {
-      const bool left = R.fleft[x];
+      const bool left = fleft[x];
 #define GEVO_LANE_OP(EXPR)                                                  \
   _Pragma("unroll") for (int h = 0; h < 4; ++h) {                           \
     const double a = left ? v[h] : o[x][h], b = left ? o[x][h] : v[h];     \
     v[h] = (EXPR);                                                          \
   }
-      switch (R.fsub[x]) {
+      switch (fsub[x]) {
         case GEVO_B_ADD: GEVO_LANE_OP(__dadd_rn(a, b)); break;
         case GEVO_B_SUB: GEVO_LANE_OP(__dsub_rn(a, b)); break;
         case GEVO_B_MUL: GEVO_LANE_OP(__dmul_rn(a, b)); break;
