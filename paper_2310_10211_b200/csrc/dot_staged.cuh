@@ -941,6 +941,202 @@ __device__ __noinline__ void dot_fast_vec(const DotArgs& dref, int col0, int col
   cp_async_wait<0>();
 }
 
+
+// Weight-update shape (K <= 32, B persistent, 32-row panels, FMA chain, fast
+// epilogue), software-pipelined: the DMMAs of panel s are issued before the
+// epilogue of panel s-1 runs, so the tensor pipe works while the previous
+// panel's operands are combined and stored.  The epilogue operands of a panel
+// are copied to registers right after its DMMAs issue (the ring slot holding
+// its full-matrix operand is refilled two panels later).
+__device__ __forceinline__ void epi_load4(const EpiR& R, int ek, const double* Es, int ers, int eks, int m,
+                                          int col0, int mm, int nn, int ncols, double (*o)[4]) {
+  const int nx = ek == EK_SELECT ? 2 : R.nops;
+#pragma unroll
+  for (int x = 0; x < kEpiPre; ++x) {
+    if (x < nx) {
+      const int src = R.src[x];
+      if (src == ES_SCALAR) {
+        const double sv = R.sval[x];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) o[x][h] = sv;
+      } else if (src == ES_TILE) {
+        const double* e = Es + mm * ers + nn * eks;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int c = (h >> 1) * 8 + (h & 1);
+          o[x][h] = nn + c < ncols ? e[c * eks] : 0.0;
+        }
+      } else {
+        const int s1 = R.st1[x];
+        const double* e = R.ptr[x] + (int64_t)m * R.st0[x] + (int64_t)(col0 + nn) * s1;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const int c = (h >> 1) * 8 + (h & 1);
+          o[x][h] = nn + c < ncols ? e[(int64_t)c * s1] : 0.0;
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void epi_apply4(const EpiR& R, int ek, double* v, const double (*o)[4]) {
+  if (ek == EK_NONE) return;
+  if (ek == EK_SELECT) {
+    const bool left = R.fleft[0];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const bool p = as_i64(o[0][h]) != 0;
+      v[h] = left ? (p ? v[h] : o[1][h]) : (p ? o[1][h] : v[h]);
+    }
+    return;
+  }
+  const int nx = R.nops;
+#pragma unroll
+  for (int x = 0; x < kEpiPre; ++x) {
+    if (x < nx) {
+      const bool left = R.fleft[x];
+#define GEVO_PIPE_OP(EXPR)                                                  \
+  _Pragma("unroll") for (int h = 0; h < 4; ++h) {                           \
+    const double a = left ? v[h] : o[x][h], b = left ? o[x][h] : v[h];     \
+    v[h] = (EXPR);                                                          \
+  }
+      switch (R.fsub[x]) {
+        case GEVO_B_ADD: GEVO_PIPE_OP(__dadd_rn(a, b)); break;
+        case GEVO_B_SUB: GEVO_PIPE_OP(__dsub_rn(a, b)); break;
+        case GEVO_B_MUL: GEVO_PIPE_OP(__dmul_rn(a, b)); break;
+        case GEVO_B_DIV: GEVO_PIPE_OP(__ddiv_rn(a, b)); break;
+        default: GEVO_PIPE_OP(np_fmax(a, b)); break;
+      }
+#undef GEVO_PIPE_OP
+    }
+  }
+}
+
+__device__ __noinline__ void dot_panels_pipe(const DotArgs& dref, int col0, int col1, double* stage_buf,
+                                             const EpiDev* epi) {
+  const DotArgs d = dref;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int M = d.M, K = d.K, ncols = col1 - col0;
+  const int ek = !epi ? EK_NONE : (epi->fast == 1 ? EK_CHAIN : EK_SELECT);
+  __shared__ EpiR R;
+  if (threadIdx.x == 0) epi_init(R, ek == EK_NONE ? nullptr : epi, true);
+  __syncthreads();
+  const bool etile = R.tile >= 0;
+  const int total = (M + kPanel - 1) / kPanel;
+  const uint32_t ring = smem_u32(stage_buf);
+  double* Bp = stage_buf + kDotStages * 2 * kTileElems;
+  VecCopy va, vx;
+  vec_init(va, d.A, d.sam, d.sak, 32 * d.sam);
+  if (etile) vec_init(vx, R.ptr[R.tile] + (int64_t)col0 * R.st1[R.tile], R.st0[R.tile], R.st1[R.tile],
+                      32 * R.st0[R.tile]);
+  else vx.kmaj = true;
+  {
+    CopyPlan pb;
+    plan_init(pb, d.B + (int64_t)col0 * d.sbn, d.sbn, d.sbk, d.b_smem, false);
+    stage(smem_u32(Bp), pb, plan_o0(pb), 0, ncols, 0, K);
+  }
+  const int brs = (d.b_smem || !(abs(d.sbk) != 0 && (d.sbn == 0 || abs(d.sbk) <= abs(d.sbn)))) ? 1 : kTS;
+  // (B's smem layout as plan_init chose it: k-major iff k is the contiguous axis)
+  const bool bkmaj = abs(d.sbk) != 0 && (d.sbn == 0 || abs(d.sbk) <= abs(d.sbn));
+  const int brs2 = bkmaj ? kTS : 1, bks = bkmaj ? 1 : kTS;
+  (void)brs;
+  const int ars = va.kmaj ? kTS : 1, aks = va.kmaj ? 1 : kTS;
+  const int ers = vx.kmaj ? kTS : 1, eks = vx.kmaj ? 1 : kTS;
+  auto load = [&](int slot, int i) {
+    const uint32_t As = ring + 8u * (slot * 2 * kTileElems);
+    const int pm = min(kPanel, M - i * kPanel);
+    vec_stage(va, As, pm, K);
+    if (etile) vec_stage(vx, As + 8u * kTileElems, pm, ncols);
+    va.p0 += va.adv;
+    vx.p0 += vx.adv;
+  };
+  load(0, 0);
+  cp_async_commit();
+  if (total > 1) load(1, 1);
+  cp_async_commit();
+
+  const int rb = warp >> 1, cb0 = (warp & 1) * 2;
+  const int lm = rb * 8 + g, ln = cb0 * 8 + 2 * t4;
+  const bool c0 = cb0 * 8 < ncols, c1 = (cb0 + 1) * 8 < ncols;
+  const int nq = K >> 2;
+  const double* pb0 = Bp + (cb0 * 8 + g) * brs2 + t4 * bks;
+  const double* pb1 = pb0 + 8 * brs2;
+  double accA[4], accB[4], eo[kEpiPre][4];
+  int slot = 0, lslot = 2;
+  bool pend = false;
+  int pm_prev = 0, m0_prev = 0;
+
+  // one panel's DMMAs (into acc) with its K tail
+  auto mma_panel = [&](double* acc, const double* As, int pm) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = 0.0;
+    if (!(c0 && rb * 8 < pm)) return;
+    const double* pa = As + lm * ars + t4 * aks;
+    const int qa = 4 * aks, qb = 4 * bks;
+    if (nq == 8 && c1) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double a = pa[q * qa];
+        dmma884(acc[0], acc[1], a, pb0[q * qb]);
+        dmma884(acc[2], acc[3], a, pb1[q * qb]);
+      }
+    } else {
+      for (int q = 0; q < nq; ++q) {
+        const double a = pa[q * qa];
+        dmma884(acc[0], acc[1], a, pb0[q * qb]);
+        if (c1) dmma884(acc[2], acc[3], a, pb1[q * qb]);
+      }
+      for (int kk = nq * 4; kk < K; ++kk) {
+        const double a = As[lm * ars + kk * aks];
+        acc[0] = fma(a, Bp[ln * brs2 + kk * bks], acc[0]);
+        acc[1] = fma(a, Bp[(ln + 1) * brs2 + kk * bks], acc[1]);
+        if (c1) {
+          acc[2] = fma(a, Bp[(ln + 8) * brs2 + kk * bks], acc[2]);
+          acc[3] = fma(a, Bp[(ln + 9) * brs2 + kk * bks], acc[3]);
+        }
+      }
+    }
+  };
+  auto emit_panel = [&](double* acc, int m0, int pm) {
+    if (!(c0 && lm < pm)) return;
+    const int m = m0 + lm;
+    epi_apply4(R, ek, acc, eo);
+    double* orow = d.out + (int64_t)m * d.som + (int64_t)(col0 + ln) * d.son;
+    const int64_t s1 = d.son, s8 = 8 * d.son;
+    if (ln < ncols) orow[0] = acc[0];
+    if (ln + 1 < ncols) orow[s1] = acc[1];
+    if (c1 && ln + 8 < ncols) orow[s8] = acc[2];
+    if (c1 && ln + 9 < ncols) orow[s8 + s1] = acc[3];
+  };
+  auto stage_body = [&](double* cur, double* prev, int s) {
+    if (s + 2 < total) load(lslot, s + 2);
+    cp_async_commit();
+    cp_async_wait<2>();
+    __syncthreads();
+    double* As = stage_buf + slot * 2 * kTileElems;
+    const int pm = min(kPanel, M - s * kPanel);
+    mma_panel(cur, As, pm);                   // tensor pipe busy ...
+    if (pend) emit_panel(prev, m0_prev, pm_prev);   // ... while panel s-1 is finished
+    if (ek != EK_NONE && c0 && lm < pm)
+      epi_load4(R, ek, As + kTileElems, ers, eks, s * kPanel + lm, col0, lm, ln, ncols, eo);
+    pend = true;
+    pm_prev = pm;
+    m0_prev = s * kPanel;
+    slot = slot == 2 ? 0 : slot + 1;
+    lslot = lslot == 2 ? 0 : lslot + 1;
+    __syncthreads();
+  };
+#pragma unroll 1
+  for (int s = 0; s < total; s += 2) {
+    stage_body(accA, accB, s);
+    if (s + 1 < total) stage_body(accB, accA, s + 1);
+  }
+  if (pend) emit_panel((total & 1) ? accA : accB, m0_prev, pm_prev);
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
 // CK: 0 FMA_CHAIN, 1 ACC8 (8 lane chains (k mod 8) per output, each on its
 // own DMMA accumulator tile, chain j's four k of a chunk (j, j+8, j+16, j+24)
 // read from the unpermuted tile with stride 8; warp = one 8x8 tile, <= 16
@@ -1335,6 +1531,7 @@ __device__ __forceinline__ void dot_columns(const DotArgs& d, int col0, int col1
       if (ck == 0 && !d.a_smem && vec_ok(d.A, d.sam, d.sak, d.M, d.K) &&
           (kstream ? (!d.b_smem && vec_ok(d.B + (int64_t)c * d.sbn, d.sbn, d.sbk, c1 - c, d.K)) : true)) {
         if (kstream) dot_fast_vec<false>(d, c, c1, stage_buf, epi);
+        else if (!epi || epi->fast != 0) dot_panels_pipe(d, c, c1, stage_buf, epi);
         else dot_fast_vec<true>(d, c, c1, stage_buf, epi);
         continue;
       }
