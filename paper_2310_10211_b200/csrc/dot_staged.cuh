@@ -837,10 +837,10 @@ __device__ __noinline__ void dot_fast_vec(const DotArgs& dref, int col0, int col
 #pragma unroll 1
   for (int s = 0; s < total; ++s) {
     GEVO_TSTAMP(ta)
-    if (s + kDotStages - 1 < total) load(s + kDotStages - 1, lslot);
-    cp_async_commit();
     GEVO_TSTAMP(tl)
-    cp_async_wait<kDotStages - 1>();
+    // stage s was committed one iteration ago (or in the prologue); the
+    // next load is issued after this stage's DMMAs so it overlaps them
+    cp_async_wait<kDotStages - 2>();
     __syncthreads();
     GEVO_TSTAMP(tb)
     GEVO_TACC(1, ta, tl)
@@ -891,6 +891,8 @@ __device__ __noinline__ void dot_fast_vec(const DotArgs& dref, int col0, int col
         }
       }
     }
+    if (s + kDotStages - 1 < total) load(s + kDotStages - 1, lslot);
+    cp_async_commit();
     GEVO_TSTAMP(tc)
     GEVO_TACC(3, tb, tc)
     if (last && ek != EK_GENERIC) {
@@ -1110,13 +1112,13 @@ __device__ __noinline__ void dot_panels_pipe(const DotArgs& dref, int col0, int 
     if (c1 && ln + 9 < ncols) orow[s8 + s1] = acc[3];
   };
   auto stage_body = [&](double* cur, double* prev, int s) {
-    if (s + 2 < total) load(lslot, s + 2);
-    cp_async_commit();
-    cp_async_wait<2>();
+    cp_async_wait<1>();                       // panel s (committed an iteration ago)
     __syncthreads();
     double* As = stage_buf + slot * 2 * kTileElems;
     const int pm = min(kPanel, M - s * kPanel);
     mma_panel(cur, As, pm);                   // tensor pipe busy ...
+    if (s + 2 < total) load(lslot, s + 2);    // ... while panel s+2 is fetched
+    cp_async_commit();
     if (pend) emit_panel(prev, m0_prev, pm_prev);   // ... while panel s-1 is finished
     if (ek != EK_NONE && c0 && lm < pm)
       epi_load4(R, ek, As + kTileElems, ers, eks, s * kPanel + lm, col0, lm, ln, ncols, eo);
