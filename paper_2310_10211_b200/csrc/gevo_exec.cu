@@ -518,7 +518,31 @@ __device__ __noinline__ void run_instrs(Shared& S, const gevo_instr* ins, int n,
   if (prof && threadIdx.x == 0) t0 = clock64();
   for (int k = 0; k < n; ++k) {
     const gevo_instr& I = ins[k];
-    switch (I.op) {
+    // small f64 binary ops with linear/scalar operands (most of a step's
+    // non-dot instructions): inline, no call
+    if (I.op == GEVO_OP_BINARY && I.kin == GEVO_K_F64 && I.sub <= GEVO_B_MAX && I.n <= 2 * kThreads &&
+        I.aux2[0] != AM_STRIDED && I.aux2[1] != AM_STRIDED && I.aux2[2] != AM_STRIDED) {
+      const int n_ = I.n, sub = I.sub;
+      const int so = I.aux2[0] == AM_LINEAR, sa = I.aux2[1] == AM_LINEAR, sb = I.aux2[2] == AM_LINEAR;
+      double* o = S.base[I.out.buf] + I.out.off;
+      const double* a = S.base[I.in[0].buf] + I.in[0].off;
+      const double* b = S.base[I.in[1].buf] + I.in[1].off;
+      const int i0 = threadIdx.x, i1 = threadIdx.x + kThreads;
+      const bool h0 = i0 < n_, h1 = i1 < n_;
+      double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
+      if (h0) { a0 = a[i0 * sa]; b0 = b[i0 * sb]; }
+      if (h1) { a1 = a[i1 * sa]; b1 = b[i1 * sb]; }
+      double r0, r1;
+      switch (sub) {
+        case GEVO_B_ADD: r0 = __dadd_rn(a0, b0); r1 = __dadd_rn(a1, b1); break;
+        case GEVO_B_SUB: r0 = __dsub_rn(a0, b0); r1 = __dsub_rn(a1, b1); break;
+        case GEVO_B_MUL: r0 = __dmul_rn(a0, b0); r1 = __dmul_rn(a1, b1); break;
+        case GEVO_B_DIV: r0 = __ddiv_rn(a0, b0); r1 = __ddiv_rn(a1, b1); break;
+        default: r0 = np_fmax(a0, b0); r1 = np_fmax(a1, b1); break;
+      }
+      if (h0) o[i0 * so] = r0;
+      if (h1) o[i1 * so] = r1;
+    } else switch (I.op) {
       case GEVO_OP_UNARY:
       case GEVO_OP_BINARY:
       case GEVO_OP_SELECT: run_elementwise(S, I); break;
