@@ -262,7 +262,7 @@ def main():
     # context; device time of the evaluation kernel (CUDA events)
     lowered_steps = []
     for s in range(total_steps):
-        lowered_steps.append([v for v in lower_all(batches[s][1], wl.config.cost_table, True)
+        lowered_steps.append([v for v in lower_all(batches[s][1], wl.config.cost_table, True, steps_cfg)
                               if v is not None])
     from paper_2310_10211_b200.plan import device_weight, layout_order, sm_aware_order
     for s in range(total_steps):

@@ -97,6 +97,10 @@ typedef struct {
   gevo_operand in[3];
 } gevo_instr;                         /* 224 bytes */
 
+/* gevo_prog.flags */
+#define GEVO_FLAG_LAYOUT_APPROX 1     /* returned layouts had no period <= 2 */
+#define GEVO_FLAG_ALTERNATE 2         /* steps >= 1: odd -> train1, even -> train0 */
+
 typedef struct {
   int32_t train0, train0_n;           /* @train_step, step 0 */
   int32_t train1, train1_n;           /* @train_step, steps >= 1 */

@@ -278,6 +278,11 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   a.progs = dp;
   a.consts = dc;
   a.arena = static_cast<double*>(ctx->arena.p);
+  // diagnostics: GEVO_POISON=1 fills every individual's arena (scratch,
+  // probs, weight ping-pong) with NaN before the launch, so a read of memory
+  // no instruction wrote shows up as a wrong result instead of stale data
+  if (getenv("GEVO_POISON"))
+    CK(cudaMemsetAsync(ctx->arena.p, 0xFF, (size_t)h->total_elems * sizeof(double), ctx->stream));
   for (int i = 0; i < GEVO_MAXP; ++i) a.wofs[i] = h->wofs[i];
   a.n_weights = h->n_weights;
   a.weight_elems = h->weight_elems;

@@ -605,13 +605,26 @@ eval_kernel(EvalArgs args) {
 
   const double* final_w = args.init_weights;
   if (args.mode == GEVO_MODE_TRAIN && args.steps > 0) {
+    // A step stores each returned weight in its numpy layout; a broadcast
+    // (stride-0) or otherwise compact return covers only part of its slot.
+    // Zero both ping-pong blocks first so the uncovered words -- not part of
+    // any weight -- are finite for the whole-block checks below.
+    for (int i = threadIdx.x; i < 2 * wsz; i += blockDim.x) wbuf[0][i] = 0.0;
+    __syncthreads();
     const gevo_instr* t0 = stage(cache, args.instrs + P.train0, P.train0_n);
     const gevo_instr* cur = t0;
     const int check = args.check_every > 0 ? args.check_every : 1;
+    const bool alternate = P.flags & GEVO_FLAG_ALTERNATE;
     for (int s = 0; s < args.steps; ++s) {
-      if (s == 1 && P.train1 != P.train0) {
+      // step 0 reads C-ordered weights (train0); later steps read the layout
+      // the previous step stored: train1 for every s >= 1, or -- when that
+      // layout flips back to C order each step (GEVO_FLAG_ALTERNATE) --
+      // train1 on odd and train0 on even steps
+      if (s >= 1 && P.train1 != P.train0 && (s == 1 || alternate)) {
+        const bool odd = s & 1;
         __syncthreads();
-        cur = stage(cache, args.instrs + P.train1, P.train1_n);
+        cur = (odd || !alternate) ? stage(cache, args.instrs + P.train1, P.train1_n)
+                                  : stage(cache, args.instrs + P.train0, P.train0_n);
       }
       const double* win = (s == 0) ? args.init_weights : wbuf[s & 1];
       double* wout = wbuf[(s + 1) & 1];
@@ -628,7 +641,7 @@ eval_kernel(EvalArgs args) {
         S.base[GEVO_BUF_PARAM0 + nw + 1] = const_cast<double*>(args.train_y) + (int64_t)b * args.y_elems;
       }
       __syncthreads();
-      run_instrs(S, cur, (s == 0) ? P.train0_n : P.train1_n, dstage, args.prof);
+      run_instrs(S, cur, (s == 0 || (alternate && !(s & 1))) ? P.train0_n : P.train1_n, dstage, args.prof);
       steps_run = s + 1;
       if ((s + 1) % check == 0 && !all_finite(wout, args.weight_elems)) {
         status = GEVO_STATUS_NONFINITE_WEIGHTS;

@@ -56,28 +56,28 @@ def _lower_pool():
 def _lower_many(batch):
     """Worker: lower a list of variants; None for a variant that fails
     (evaluate() maps any exception to INVALID_FITNESS)."""
-    fns_list, cost_table, training = batch
+    fns_list, cost_table, training, steps = batch
     out = []
     for fns in fns_list:
         try:
-            out.append(lower_variant(fns, cost_table, training=training))
+            out.append(lower_variant(fns, cost_table, training=training, steps=steps))
         except Exception:
             out.append(None)
     return out
 
 
-def _submit_lowering(variants, idx, cost_table, training):
+def _submit_lowering(variants, idx, cost_table, training, steps=600):
     """Start lowering variants[idx] (None entries excluded by the caller).
     Returns a list of (positions, future-or-result) in idx order."""
     pool = _lower_pool() if len(idx) >= POOL_MIN else None
     if pool is None:
-        return [(list(idx), _lower_many(([variants[i] for i in idx], cost_table, training)))]
+        return [(list(idx), _lower_many(([variants[i] for i in idx], cost_table, training, steps)))]
     nw = pool._max_workers
     per = max(4, (len(idx) + 2 * nw - 1) // (2 * nw))
     out = []
     for k in range(0, len(idx), per):
         c = idx[k:k + per]
-        out.append((c, pool.submit(_lower_many, ([variants[i] for i in c], cost_table, training))))
+        out.append((c, pool.submit(_lower_many, ([variants[i] for i in c], cost_table, training, steps))))
     return out
 
 
@@ -89,12 +89,12 @@ def _collect(jobs):
     return pos, res
 
 
-def lower_all(variants, cost_table, training):
+def lower_all(variants, cost_table, training, steps=600):
     """lower_variant over a list (None entries stay None), in the process
     pool when the list is large."""
     idx = [i for i, v in enumerate(variants) if v is not None]
     out = [None] * len(variants)
-    for i, r in zip(*_collect(_submit_lowering(variants, idx, cost_table, training))):
+    for i, r in zip(*_collect(_submit_lowering(variants, idx, cost_table, training, steps))):
         out[i] = r
     return out
 
@@ -198,7 +198,7 @@ class DeviceEvaluator:
         halves = [idx]
         if len(idx) >= 2 * POOL_MIN and _lower_pool() is not None:
             halves = [idx[:len(idx) // 2], idx[len(idx) // 2:]]
-        jobs = [_submit_lowering(variants, h, cfg.cost_table, training) for h in halves]
+        jobs = [_submit_lowering(variants, h, cfg.cost_table, training, cfg.steps) for h in halves]
         ctxs = [self.ctx, self._second_context() if len(halves) > 1 else None]
         runner, box = None, {}
         t_lower = t_pack = 0.0

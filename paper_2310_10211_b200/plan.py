@@ -12,7 +12,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import layout as L
-from .lowering import (BUF_OUT0, FLAG_LAYOUT_APPROX, HEADER_DTYPE,
+from .lowering import (BUF_OUT0, FLAG_ALTERNATE, FLAG_LAYOUT_APPROX, HEADER_DTYPE,
                        INSTR_DTYPE, PLAN_MAGIC, PLAN_VERSION, PROG_DTYPE,
                        consts_to_words, encode_instrs, lower_function,
                        static_cost)
@@ -41,10 +41,11 @@ def _count(shape):
 
 
 def lower_variant(functions: dict, cost_table=None, training=True,
-                  weight_layouts=None) -> VariantPlan:
+                  weight_layouts=None, steps: int = 600) -> VariantPlan:
     """functions: {'train_step': fn, 'forward': fn} (train_step only in
     training mode).  Weight params start C-ordered like the module
-    constants; steps >= 1 see the layout the previous step stored."""
+    constants; steps >= 1 see the layout the previous step stored, and
+    @forward is lowered for the layout after `steps` training steps."""
     consts: list = []
     arena = 0
     smem = 0
@@ -58,23 +59,34 @@ def lower_variant(functions: dict, cost_table=None, training=True,
         c_layout = [L.c_strides(tuple(t.shape)) for _, t in ts.params]
         low0 = lower_function(ts, c_layout, cost_table=cost_table)
         train_cost = low0.cost
-        layouts = list(c_layout)
-        layouts[:nw] = low0.ret_strides
-        if tuple(low0.ret_strides) == tuple(c_layout[:nw]):
-            low1 = low0
+        L0 = list(low0.ret_strides)
+        final = L0                          # layout of the weights after `steps`
+        if L0 == list(c_layout[:nw]):
+            low1 = low0                     # C order is a fixed point
         else:
+            layouts = list(c_layout)
+            layouts[:nw] = L0
             low1 = lower_function(ts, layouts, cost_table=cost_table)
-            if tuple(low1.ret_strides) != tuple(low0.ret_strides):
-                # a second change: take the layout after step 1 for all
-                # later steps and flag it (never seen on the MLP workloads)
-                layouts[:nw] = low1.ret_strides
+            L1 = list(low1.ret_strides)
+            if L1 == L0:
+                final = L0                  # fixed point from step 1 on
+            elif L1 == list(c_layout[:nw]):
+                # period 2: even steps read C order (train0) and store L0,
+                # odd steps read L0 (train1) and store C order
+                flags |= FLAG_ALTERNATE
+                final = L0 if (steps - 1) % 2 == 0 else L1
+            else:
+                # no period <= 2 (never seen): later steps approximated by
+                # the layout after step 1, and the individual flagged
+                layouts[:nw] = L1
                 low1 = lower_function(ts, layouts, cost_table=cost_table)
                 flags |= FLAG_LAYOUT_APPROX
+                final = list(low1.ret_strides)
         t0 = _encode_shifted(low0, consts)
         t1 = t0 if low1 is low0 else _encode_shifted(low1, consts)
         arena = max(low0.arena_elems, low1.arena_elems)
         smem = max(low0.smem_elems, low1.smem_elems)
-        fwd_layouts = list(low1.ret_strides)
+        fwd_layouts = final if steps > 0 else list(c_layout[:nw])
     fw = functions["forward"]
     nwf = len(fw.params) - 1
     f_layout = [L.c_strides(tuple(t.shape)) for _, t in fw.params]

@@ -83,7 +83,7 @@ def test_pool_lowering_matches_in_process():
     inds = load("train_pop.json.gz")["individuals"][:70]
     variants = [variant_functions(i) for i in inds]
     a = E.lower_all(variants, None, True)             # pool (>= POOL_MIN)
-    b = E._lower_many((variants, None, True))         # in-process
+    b = E._lower_many((variants, None, True, 600))    # in-process
     for x, y in zip(a, b):
         assert x.train_cost == y.train_cost and x.fwd_cost == y.fwd_cost
         assert x.train0.tobytes() == y.train0.tobytes()

@@ -136,6 +136,36 @@ def test_train_population_fitness(train_wl):
     assert exact >= 0.9 * len(inds)
 
 
+def test_bench_pool_fitness_at_full_size():
+    """Every fresh individual of the recorded pop-256 x 10-generation run
+    (the bench pool, BASELINE.json configs[1]) at the full default workload
+    -- 600 steps, 31 scored batches -- against the fitness the reference
+    recorded for it (tests/golden/make_golden.py --bench)."""
+    from paper_2310_10211_b200.dialect import parse_function
+    inds = [i for i in load("bench_train_pool.json.gz")["individuals"] if not i.get("invalid_patch")]
+    seen, pool = set(), []
+    for i in inds:
+        if i["key"] not in seen:
+            seen.add(i["key"])
+            pool.append(i)
+    wl = W.build_2fcnet_workload()
+    ev = DeviceEvaluator(wl)
+    variants = [{k: parse_function(i[k]) for k in ("forward", "train_step")} for i in pool]
+    fits = []
+    for c in range(0, len(variants), 512):
+        fits += ev.evaluate_variants(variants[c:c + 512])
+    ev.close()
+    exact, off = 0, []
+    for k, (f, i) in enumerate(zip(fits, pool)):
+        assert f.cost == i["cost"]
+        assert (f.error == 1.0) == (i["error"] == 1.0)
+        exact += f.error == i["error"]
+        if f.error != i["error"]:
+            off.append((k, f.error, i["error"]))
+    print(f"bench pool (full size) error bit-exact {exact}/{len(pool)}; differing {off}")
+    assert exact == len(pool)
+
+
 def test_baseline_and_gradient_patch(train_wl):
     meta = load("meta.json")["baseline"]["train2fc"]
     g = load("train_pop.json.gz")["gradient_scaling"]
