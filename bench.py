@@ -255,6 +255,7 @@ def main():
         torch.cuda.synchronize()
 
     kern_ms, wall_s, alg_bytes, alg_flops, h2d, d2h = [], [], [], [], [], []
+    parity_ok = parity_n = 0
     from paper_2310_10211_b200.evaluator import lower_all
     from paper_2310_10211_b200.plan import build_population_plan
     clocks = Clocks(local)
@@ -300,6 +301,10 @@ def main():
             wall_s.append(t1 - t0)
             h2d.append(int(ev.last_plan_bytes))
             d2h.append(args.pop * 24)
+            # the pool records the reference's own fitness for every variant
+            for f, ind in zip(fits, sel):
+                parity_n += 1
+                parity_ok += (f.cost, f.error) == (ind["cost"], ind["error"])
     barrier()
     ck = clocks.stop()
     dev_s = sum(kern_ms) / 1000.0
@@ -354,6 +359,8 @@ def main():
                          "fp64_tflops": statistics.mean(alg_flops) / per_launch_s / 1e12},
             "cpu_baseline": cpu,
             "clocks": ck,
+            "parity": {"bit_exact": parity_ok, "of": parity_n,
+                       "against": "reference (cost, error) recorded in the bench pool"},
         }
         print(json.dumps(line), flush=True)
     ev.close()
