@@ -22,6 +22,9 @@
  *                                   crowding_distance :123-140
  *   gevo_nsga2_crowding          -- crowding_distance (search.py:123-140)
  *   gevo_nsga2_select            -- select_survivors (search.py:163-179)
+ *   gevo_archive_merge           -- Archive.offer (search.py:208-228) for a
+ *                                   batch of offers with new keys
+ *   gevo_hypervolume             -- hypervolume (search.py:182-195)
  *   gevo_last_error              -- (Python exceptions in the reference)
  *   gevo_profile                 -- (no analogue: per-instruction-class
  *                                   cycle counters for diagnostics)
@@ -122,6 +125,19 @@ int gevo_nsga2_rank(gevo_ctx* ctx, const double* cost, const double* error,
                     int n, int32_t* rank, double* crowding,
                     int32_t* front_order, int32_t* front_start,
                     int32_t* n_fronts);
+
+/* Archive.offer (search.py:208-228) of a whole batch: points 0..n-1 are the
+ * archive entries in order followed by the batch's valid offers in offer
+ * order, all with keys that are not in the archive and not repeated in the
+ * batch (the caller splits a batch at a repeated key; search.py:211).
+ * keep[0..*n_keep) = indices of the resulting entries, in archive order;
+ * identical to offering the batch one point at a time.  keep holds n ints. */
+int gevo_archive_merge(gevo_ctx* ctx, const double* cost, const double* error,
+                       int n, int32_t* keep, int32_t* n_keep);
+
+/* hypervolume(points, ref) (search.py:182-195), bit-identical */
+int gevo_hypervolume(gevo_ctx* ctx, const double* cost, const double* error,
+                     int n, double ref_cost, double ref_error, double* out);
 
 /* crowding_distance (search.py:123-140) of points taken as ONE front
  * (ties on an axis break by position) */

@@ -65,6 +65,10 @@ SIGNATURES = {
                                            c_dblp]),
     "gevo_nsga2_select": (ctypes.c_int, [ctypes.c_void_p, c_dblp, c_dblp, ctypes.c_int,
                                          ctypes.c_int, c_i32p, c_i32p, c_dblp]),
+    "gevo_archive_merge": (ctypes.c_int, [ctypes.c_void_p, c_dblp, c_dblp, ctypes.c_int,
+                                          c_i32p, c_i32p]),
+    "gevo_hypervolume": (ctypes.c_int, [ctypes.c_void_p, c_dblp, c_dblp, ctypes.c_int,
+                                        ctypes.c_double, ctypes.c_double, c_dblp]),
 }
 
 _lib = None
@@ -230,3 +234,24 @@ class Context:
             self.h, ptr(cost), ptr(err), n, keep, ptr(chosen, ctypes.c_int32),
             ptr(rank, ctypes.c_int32), ptr(crowd)), "nsga2_select")
         return chosen[:keep], rank[:n], crowd[:n]
+
+    def archive_merge(self, cost, err):
+        """Indices kept when the points after the archive's are offered in
+        order (gevo_archive_merge)."""
+        cost = np.ascontiguousarray(cost, dtype=np.float64)
+        err = np.ascontiguousarray(err, dtype=np.float64)
+        keep = np.zeros(max(cost.size, 1), dtype=np.int32)
+        nk = ctypes.c_int32()
+        self.check(self.lib.gevo_archive_merge(self.h, ptr(cost), ptr(err), cost.size,
+                                               ptr(keep, ctypes.c_int32), ctypes.byref(nk)),
+                   "archive_merge")
+        return keep[:nk.value]
+
+    def hypervolume(self, cost, err, ref):
+        cost = np.ascontiguousarray(cost, dtype=np.float64)
+        err = np.ascontiguousarray(err, dtype=np.float64)
+        out = np.zeros(1)
+        self.check(self.lib.gevo_hypervolume(self.h, ptr(cost), ptr(err), cost.size,
+                                             float(ref[0]), float(ref[1]), ptr(out)),
+                   "hypervolume")
+        return float(out[0])

@@ -450,6 +450,68 @@ static int nsga2_common(gevo_ctx* ctx, const double* cost, const double* error, 
   return GEVO_OK;
 }
 
+int gevo_archive_merge(gevo_ctx* ctx, const double* cost, const double* error, int n,
+                       int32_t* keep, int32_t* n_keep) {
+  if (!ctx) return GEVO_E_ARG;
+  if (n < 0 || (n > 0 && (!cost || !error || !keep)) || !n_keep)
+    return fail(ctx, GEVO_E_ARG, "bad archive_merge arguments");
+  *n_keep = 0;
+  if (n == 0) return GEVO_OK;
+  CK(cudaSetDevice(ctx->device));
+  if (ctx->ns.ensure(2 * (size_t)n * 8 + ((size_t)n + 2) * 4 + 64))
+    return fail(ctx, GEVO_E_CUDA, "archive alloc failed");
+  double* d = static_cast<double*>(ctx->ns.p);
+  int32_t* iv = reinterpret_cast<int32_t*>(d + 2 * (size_t)n);
+  ArchArgs a;
+  a.n = n;
+  a.c = d;
+  a.e = d + n;
+  a.keep = iv;
+  a.n_keep = iv + n;
+  CK(cudaMemcpyAsync(d, cost, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d + n, error, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  launch_archive_merge(a, ctx->stream);
+  CK(cudaGetLastError());
+  int32_t k = 0;
+  CK(cudaMemcpyAsync(&k, a.n_keep, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (k < 0 || k > n) return fail(ctx, GEVO_E_CUDA, "archive merge returned a bad count");
+  if (k) CK(cudaMemcpy(keep, a.keep, (size_t)k * 4, cudaMemcpyDeviceToHost));
+  *n_keep = k;
+  return GEVO_OK;
+}
+
+int gevo_hypervolume(gevo_ctx* ctx, const double* cost, const double* error, int n,
+                     double ref_cost, double ref_error, double* out) {
+  if (!ctx) return GEVO_E_ARG;
+  if (n < 0 || (n > 0 && (!cost || !error)) || !out)
+    return fail(ctx, GEVO_E_ARG, "bad hypervolume arguments");
+  *out = 0.0;
+  if (n == 0) return GEVO_OK;
+  CK(cudaSetDevice(ctx->device));
+  if (ctx->ns.ensure((5 * (size_t)n + 1) * 8 + (size_t)n * 4 + 64))
+    return fail(ctx, GEVO_E_CUDA, "hypervolume alloc failed");
+  double* d = static_cast<double*>(ctx->ns.p);
+  HvArgs a;
+  a.n = n;
+  a.c = d;
+  a.e = d + n;
+  a.sc = d + 2 * (size_t)n;
+  a.se = d + 3 * (size_t)n;
+  a.area = d + 4 * (size_t)n;
+  a.out = d + 5 * (size_t)n;
+  a.flag = reinterpret_cast<int32_t*>(d + 5 * (size_t)n + 1);
+  a.ref_c = ref_cost;
+  a.ref_e = ref_error;
+  CK(cudaMemcpyAsync(d, cost, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d + n, error, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  launch_hypervolume(a, ctx->stream);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, a.out, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return GEVO_OK;
+}
+
 int gevo_nsga2_rank(gevo_ctx* ctx, const double* cost, const double* error, int n,
                     int32_t* rank, double* crowding, int32_t* front_order,
                     int32_t* front_start, int32_t* n_fronts) {

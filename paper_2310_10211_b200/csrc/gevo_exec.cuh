@@ -61,4 +61,28 @@ struct NsArgs {
 
 void launch_nsga2(const NsArgs& a, cudaStream_t st);
 
+// Archive merge and hypervolume (nsga2.cu)
+struct ArchArgs {
+  int n;
+  const double* c;
+  const double* e;
+  int32_t* keep;      // [n] kept indices in order
+  int32_t* n_keep;    // [1]
+};
+
+struct HvArgs {
+  int n;
+  const double* c;
+  const double* e;
+  double ref_c, ref_e;
+  double* sc;         // scratch [n] inside points in sweep order
+  double* se;         // scratch [n]
+  double* area;       // scratch [n] step areas
+  int32_t* flag;      // scratch [n] the point steps the ceiling down
+  double* out;        // [1]
+};
+
+void launch_archive_merge(const ArchArgs& a, cudaStream_t st);
+void launch_hypervolume(const HvArgs& a, cudaStream_t st);
+
 }  // namespace gevo

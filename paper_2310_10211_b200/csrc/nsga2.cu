@@ -10,6 +10,7 @@
 //                                 then axis 1, one IEEE rounding each)
 //   select_survivors   :163-179 (whole fronts, then the partial front by
 //                                 (-crowding, index))
+//   hypervolume        :182-195 and the Archive merge :208-228 (below)
 // One CTA of 1024 threads; O(n^2) dominance work spread over the CTA, all
 // sorts are counting sorts on unique (key, index) pairs, no float atomics.
 #include <cuda_runtime.h>
@@ -184,6 +185,144 @@ __global__ void __launch_bounds__(kNsThreads) nsga2_kernel(NsArgs a) {
 
 void launch_nsga2(const NsArgs& a, cudaStream_t st) {
   nsga2_kernel<<<1, kNsThreads, 0, st>>>(a);
+}
+
+// ---------------------------------------------------------------------------
+// Archive merge (search.py:208-228, batched).  Points 0..n_old-1 are the
+// archive entries in order, the rest one batch of valid offers in offer
+// order whose keys are all new (the host splits batches at key repeats).
+// Offering them one by one keeps exactly the points that nothing in the
+// list dominates and that no EARLIER point equals (an equal or dominating
+// point reaching the archive first blocks it; anything that later evicts
+// that blocker dominates it too), in list order -- which is the order
+// `kept + [new]` leaves them in.  O(n^2) compares over the CTA, order kept
+// by a block scan.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kNsThreads) archive_merge_kernel(ArchArgs a) {
+  __shared__ int tmp[32];
+  const int n = a.n;
+  const double* C = a.c;
+  const double* E = a.e;
+  int base = 0;
+  for (int j0 = 0; j0 < n; j0 += blockDim.x) {
+    const int j = j0 + threadIdx.x;
+    int keep = 0;
+    if (j < n) {
+      const double cj = C[j], ej = E[j];
+      keep = 1;
+      for (int i = 0; i < n; ++i) {
+        const double ci = C[i], ei = E[i];
+        if (dom(ci, ei, cj, ej) || (i < j && ci == cj && ei == ej)) { keep = 0; break; }
+      }
+    }
+    int total;
+    const int pos = block_scan(keep, tmp, &total);
+    if (keep) a.keep[base + pos] = j;
+    base += total;
+  }
+  if (threadIdx.x == 0) *a.n_keep = base;
+}
+
+// block-wide exclusive running minimum (kNsThreads threads, one item each);
+// min is exact, so any association gives the sequential result
+__device__ double block_min_scan(double v, double init, double* tmp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x = fmin(x, y);
+  }
+  if (lane == 31) tmp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    double w = lane < (kNsThreads / 32) ? tmp[lane] : INFINITY;
+    for (int o = 1; o < 32; o <<= 1) {
+      double y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w = fmin(w, y);
+    }
+    tmp[lane] = w;
+  }
+  __syncthreads();
+  double excl = __shfl_up_sync(0xffffffffu, x, 1);
+  if (lane == 0) excl = INFINITY;
+  if (warp > 0) excl = fmin(excl, tmp[warp - 1]);
+  excl = fmin(excl, init);
+  __syncthreads();
+  return excl;
+}
+
+// ---------------------------------------------------------------------------
+// Hypervolume (search.py:182-195).  The points strictly inside the corner
+// are placed in (cost, error) order by counting (ties by index, as the
+// stable sort leaves them).  The running ceiling before each point is an
+// exclusive min-scan, and each step's area is one IEEE subtract/subtract/
+// multiply.  One thread then adds the stepping points' areas in sweep order,
+// as the reference's `total +=` does.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kNsThreads) hypervolume_kernel(HvArgs a) {
+  __shared__ int tmp[32];
+  __shared__ double dtmp[32];
+  const int n = a.n;
+  const double* C = a.c;
+  const double* E = a.e;
+  const double r0 = a.ref_c, r1 = a.ref_e;
+  int m = 0;
+  // 1. inside points, counted into sweep positions
+  for (int j0 = 0; j0 < n; j0 += blockDim.x) {
+    const int p = j0 + threadIdx.x;
+    int in = 0;
+    double cp = 0, ep = 0;
+    if (p < n) {
+      cp = C[p];
+      ep = E[p];
+      in = cp < r0 && ep < r1;
+    }
+    int total;
+    block_scan(in, tmp, &total);
+    m += total;
+    if (!in) continue;
+    int pos = 0;
+    for (int q = 0; q < n; ++q) {
+      const double cq = C[q], eq = E[q];
+      if (!(cq < r0 && eq < r1)) continue;
+      pos += cq < cp || (cq == cp && (eq < ep || (eq == ep && q < p)));
+    }
+    a.sc[pos] = cp;
+    a.se[pos] = ep;
+  }
+  __syncthreads();
+  // 2. ceiling before each position and the step areas
+  double ceil_carry = r1;
+  for (int k0 = 0; k0 < m; k0 += blockDim.x) {
+    const int k = k0 + threadIdx.x;
+    const double e = k < m ? a.se[k] : INFINITY;
+    const double ceil = block_min_scan(e, ceil_carry, dtmp);
+    if (k < m) {
+      const bool step = e < ceil;
+      a.area[k] = step ? __dmul_rn(__dsub_rn(r0, a.sc[k]), __dsub_rn(ceil, e)) : 0.0;
+      a.flag[k] = step;
+    }
+    // carry = min over this chunk, via the last thread's inclusive value
+    if (threadIdx.x == blockDim.x - 1) dtmp[0] = fmin(ceil, e);
+    __syncthreads();
+    ceil_carry = dtmp[0];
+    __syncthreads();
+  }
+  // 3. the sequential sum
+  if (threadIdx.x == 0) {
+    double total = 0.0;
+    for (int k = 0; k < m; ++k)
+      if (a.flag[k]) total = __dadd_rn(total, a.area[k]);
+    *a.out = total;
+  }
+}
+
+void launch_archive_merge(const ArchArgs& a, cudaStream_t st) {
+  archive_merge_kernel<<<1, kNsThreads, 0, st>>>(a);
+}
+
+void launch_hypervolume(const HvArgs& a, cudaStream_t st) {
+  hypervolume_kernel<<<1, kNsThreads, 0, st>>>(a);
 }
 
 }  // namespace gevo

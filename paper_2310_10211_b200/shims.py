@@ -14,9 +14,11 @@ so rebinding the module attributes is the only non-invasive plug-in point):
   evotir.search.crowding_distance   -> crowding_distance   (search.py:123-140)
   evotir.search.rank_population     -> rank_population     (search.py:143-150)
   evotir.search.select_survivors    -> select_survivors    (search.py:163-179)
+  evotir.search.hypervolume         -> hypervolume         (search.py:182-195)
+  evotir.search.Archive             -> Archive             (search.py:202-233)
 
 Everything else -- IR, apply_patch, mutation/crossover, the RNG, the search
-loop, archive, artifacts -- stays the reference's own code.  Results are the
+loop, artifacts -- stays the reference's own code.  Results are the
 reference's Fitness objects; the device computes f32 programs in float64 with
 the reference's summation orders ("Parity").
 
@@ -250,6 +252,114 @@ def select_survivors(pool, n):
 
 
 # ---------------------------------------------------------------------------
+# Archive and hypervolume on the device
+# ---------------------------------------------------------------------------
+
+def hypervolume(points, ref):
+    """Area dominated by `points` and bounded by the reference corner
+    (search.py:182-195), bit-identical (gevo_hypervolume)."""
+    if len(points) == 0:
+        return 0.0
+    c, e = _arrays(points)
+    return _ns_ctx().hypervolume(c, e, ref)
+
+
+def _archive_entry_type():
+    try:
+        from evotir.search import ArchiveEntry
+        return ArchiveEntry
+    except ImportError:      # tests without the reference package
+        from dataclasses import dataclass
+
+        @dataclass
+        class ArchiveEntry:
+            patch: tuple
+            fitness: object
+            holdout: object = None
+        return ArchiveEntry
+
+
+class Archive:
+    """Drop-in for search.Archive (search.py:202-233): the globally
+    non-dominated (patch, fitness) set, first comer keeping a point.
+
+    `offer` queues; the queue is merged on the device in one pass
+    (gevo_archive_merge) when `entries`, `_keys` or `sorted_entries` are next
+    read -- once per generation under run_search (absorb, then record:
+    search.py:350-368) instead of O(archive) Python work per evaluation.
+    A queued batch must hold only keys that are new at the time of offer for
+    the one-pass result to equal sequential offering, so an offer whose key
+    is known (in the archive or already queued) first flushes the queue and
+    then takes the reference's key check (search.py:211) against the exact
+    archive.  `merge=` substitutes the device in host tests.
+    """
+
+    def __init__(self, merge=None):
+        self._entries = []
+        self._ekeys = []          # the offer key of each entry
+        self._keyset = set()
+        self._pending = []        # (patch, fitness, key)
+        self._pkeys = set()
+        self._merge = merge
+        self._Entry = _archive_entry_type()
+
+    def offer(self, patch, fitness, key):
+        if not fitness.valid:
+            return
+        if key in self._pkeys or key in self._keyset:
+            self._flush()
+            if key in self._keyset:
+                return
+        self._pending.append((patch, fitness, key))
+        self._pkeys.add(key)
+
+    def _flush(self):
+        if not self._pending:
+            return
+        pend, self._pending, self._pkeys = self._pending, [], set()
+        pts = [e.fitness.as_tuple() for e in self._entries] + [f.as_tuple() for _, f, _ in pend]
+        c, e = _arrays(pts)
+        merge = self._merge or _ns_ctx().archive_merge
+        n_old = len(self._entries)
+        entries, keys = [], []
+        for j in merge(c, e):
+            j = int(j)
+            if j < n_old:
+                entries.append(self._entries[j])
+                keys.append(self._ekeys[j])
+            else:
+                patch, fit, key = pend[j - n_old]
+                entries.append(self._Entry(patch=patch, fitness=fit))
+                keys.append(key)
+        self._entries, self._ekeys, self._keyset = entries, keys, set(keys)
+
+    @property
+    def entries(self):
+        self._flush()
+        return self._entries
+
+    @entries.setter
+    def entries(self, value):
+        _, G, _ = _E()
+        self._pending, self._pkeys = [], set()
+        self._entries = list(value)
+        self._ekeys = [G.patch_dumps(e.patch) for e in self._entries]
+        self._keyset = set(self._ekeys)
+
+    @property
+    def _keys(self):
+        self._flush()
+        return self._keyset
+
+    def sorted_entries(self):
+        self._flush()
+        order = sorted(range(len(self._entries)),
+                       key=lambda i: (self._entries[i].fitness.cost,
+                                      self._entries[i].fitness.error, self._ekeys[i]))
+        return [self._entries[i] for i in order]
+
+
+# ---------------------------------------------------------------------------
 
 _SAVED: dict = {}
 
@@ -269,6 +379,8 @@ def install(device: int = 0, nsga2: bool = True):
             ("search", "crowding_distance"): S.crowding_distance,
             ("search", "rank_population"): S.rank_population,
             ("search", "select_survivors"): S.select_survivors,
+            ("search", "hypervolume"): S.hypervolume,
+            ("search", "Archive"): S.Archive,
         })
 
     class _Bound(GpuEvaluator):
@@ -283,6 +395,8 @@ def install(device: int = 0, nsga2: bool = True):
         S.crowding_distance = crowding_distance
         S.rank_population = rank_population
         S.select_survivors = select_survivors
+        S.hypervolume = hypervolume
+        S.Archive = Archive
 
 
 def uninstall():

@@ -58,18 +58,30 @@ def test_gpu_evaluator_seam_reproduces_recorded_search():
         def __init__(self, workload):
             super().__init__(workload, backend=backend)
 
+    # the queueing Archive seam too, its one-pass merge stated by the oracle
+    # (the device kernel is checked against the same rule in test_archive.py)
+    from oracle import archive as OA
+
+    class QArchive(shims.Archive):
+        def __init__(self):
+            super().__init__(merge=lambda c, e: OA.merge_batch(list(zip(c.tolist(),
+                                                                        e.tolist()))))
+
+    saved = (S.Archive, S.hypervolume)
     S._Evaluator = Seam
+    S.Archive, S.hypervolume = QArchive, OA.hypervolume
     try:
         w = F.build_2fcnet_workload()
         cfg = S.SearchConfig(**data["config"])
         res = S.run_search(w, cfg)
     finally:
         S._Evaluator = orig
+        S.Archive, S.hypervolume = saved
     assert res.evaluations == len(data["individuals"])
-    got = [{k: h[k] for k in ("generation", "evaluations", "front_size", "best_error",
-                              "best_cost", "archive_size")} for h in res.history]
-    want = [{k: h[k] for k in ("generation", "evaluations", "front_size", "best_error",
-                               "best_cost", "archive_size")} for h in data["history"]]
+    keys = ("generation", "evaluations", "front_size", "best_error", "best_cost",
+            "archive_size", "hypervolume", "archive_hypervolume")
+    got = [{k: h[k] for k in keys} for h in res.history]
+    want = [{k: h[k] for k in keys} for h in data["history"]]
     assert got == want
     # one device call per evaluator call (baseline, initial, each generation)
     assert len(backend.calls) == 1 + 1 + data["config"]["generations"]
@@ -88,6 +100,7 @@ def test_install_rebinds_and_restores():
         assert S.holdout_report is shims.holdout_report
         assert S.select_survivors is shims.select_survivors
         assert S.nondominated_sort is shims.nondominated_sort
+        assert S.Archive is shims.Archive and S.hypervolume is shims.hypervolume
     finally:
         shims.uninstall()
     assert (S._Evaluator, S.evaluate, C.holdout_report, S.select_survivors) == before
