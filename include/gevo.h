@@ -9,6 +9,13 @@
  *   gevo_upload_split            -- SplitView.whole_batches
  *                                   (pkg/src/evotir/datasets.py:149-162),
  *                                   uploaded once instead of per evaluation
+ *   gevo_upload_split_u8         -- read_idx_images / load_dataset scaling
+ *                                   (datasets.py:33-45,187-192) +
+ *                                   whole_batches: raw pixel bytes decoded
+ *                                   on the device
+ *   gevo_upload_split_cifar      -- (new, CNN workload A24) CIFAR-10 binary
+ *                                   records decoded to NHWC on the device
+ *   gevo_download_split          -- (no analogue: reads a split back)
  *   gevo_upload_weights          -- module.constants[w1,b1,w2,b2]
  *                                   (fitness.py:341, fitness.py:388)
  *   gevo_eval                    -- evaluate() for a list of variants
@@ -102,6 +109,25 @@ const char* gevo_last_error(gevo_ctx* ctx);
 int gevo_upload_split(gevo_ctx* ctx, int split_id, const double* x, int64_t n,
                       int features, const int64_t* labels, int classes,
                       int batch);
+
+/* Same split from raw pixel bytes (n x features uint8): x = u8 / 255.0 is
+ * computed on the device, bit-identical to u8.astype(float64) / 255.0
+ * (datasets.py:44,192). */
+int gevo_upload_split_u8(gevo_ctx* ctx, int split_id, const uint8_t* pixels,
+                         int64_t n, int features, const int64_t* labels,
+                         int classes, int batch);
+
+/* CIFAR-10 binary records, each [label u8][channels planes of side*side u8];
+ * decoded on the device to NHWC rows x = u8 / 255.0 (features =
+ * side*side*channels) plus labels and one-hot targets. */
+int gevo_upload_split_cifar(gevo_ctx* ctx, int split_id, const uint8_t* records,
+                            int64_t n, int channels, int side, int classes,
+                            int batch);
+
+/* Copy a split's device arrays back (any pointer may be NULL); *rows = the
+ * number of rows kept (whole batches). */
+int gevo_download_split(gevo_ctx* ctx, int split_id, double* x, double* y,
+                        int64_t* labels, int64_t* rows);
 
 /* concatenated initial (training) or frozen (prediction) weight arrays,
  * C order, in @train_step return order */

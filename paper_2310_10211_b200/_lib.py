@@ -65,6 +65,14 @@ SIGNATURES = {
                                            c_dblp]),
     "gevo_nsga2_select": (ctypes.c_int, [ctypes.c_void_p, c_dblp, c_dblp, ctypes.c_int,
                                          ctypes.c_int, c_i32p, c_i32p, c_dblp]),
+    "gevo_upload_split_u8": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                            ctypes.c_int64, ctypes.c_int, c_i64p, ctypes.c_int,
+                                            ctypes.c_int]),
+    "gevo_upload_split_cifar": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                               ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                               ctypes.c_int, ctypes.c_int]),
+    "gevo_download_split": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, c_dblp, c_dblp,
+                                           c_i64p, c_i64p]),
     "gevo_archive_merge": (ctypes.c_int, [ctypes.c_void_p, c_dblp, c_dblp, ctypes.c_int,
                                           c_i32p, c_i32p]),
     "gevo_hypervolume": (ctypes.c_int, [ctypes.c_void_p, c_dblp, c_dblp, ctypes.c_int,
@@ -156,6 +164,36 @@ class Context:
         self.check(self.lib.gevo_upload_split(self.h, split_id, ptr(x), n, f,
                                               ptr(labels, ctypes.c_int64),
                                               classes, batch), "upload_split")
+
+    def upload_split_u8(self, split_id, pixels, labels, classes, batch):
+        """x = pixels / 255.0 decoded on the device (pixels: n x F uint8)."""
+        pixels = np.ascontiguousarray(pixels, dtype=np.uint8)
+        labels = np.ascontiguousarray(labels, dtype=np.int64)
+        n, f = pixels.shape
+        self.check(self.lib.gevo_upload_split_u8(self.h, split_id, pixels.ctypes.data, n, f,
+                                                 ptr(labels, ctypes.c_int64), classes, batch),
+                   "upload_split_u8")
+
+    def upload_split_cifar(self, split_id, records, channels, side, classes, batch):
+        """CIFAR-10 binary records (n x (1 + C*side*side) uint8)."""
+        records = np.ascontiguousarray(records, dtype=np.uint8)
+        n = records.shape[0]
+        if records.shape[1] != 1 + channels * side * side:
+            raise GevoError("CIFAR record size does not match channels/side")
+        self.check(self.lib.gevo_upload_split_cifar(self.h, split_id, records.ctypes.data, n,
+                                                    channels, side, classes, batch),
+                   "upload_split_cifar")
+
+    def download_split(self, split_id, features, classes, max_rows):
+        x = np.zeros((max(max_rows, 1), features))
+        y = np.zeros((max(max_rows, 1), classes))
+        lb = np.zeros(max(max_rows, 1), dtype=np.int64)
+        rows = ctypes.c_int64()
+        self.check(self.lib.gevo_download_split(self.h, split_id, ptr(x), ptr(y),
+                                                ptr(lb, ctypes.c_int64), ctypes.byref(rows)),
+                   "download_split")
+        r = rows.value
+        return x[:r], y[:r], lb[:r]
 
     def upload_weights(self, flat):
         flat = np.ascontiguousarray(flat, dtype=np.float64)

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libgevo.so")
-SOURCES = ["gevo_exec.cu", "nsga2.cu", "gevo_abi.cu"]
+SOURCES = ["gevo_exec.cu", "nsga2.cu", "splits.cu", "gevo_abi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -52,6 +52,9 @@ class CnnConfig:
     data_seed: int = 11
     init_seed: int = 4321
     cost_table: dict = field(default_factory=dict)
+    # CIFAR-10 binary batch files (datasets.read_cifar_bin) instead of the
+    # synthetic images: search = the first search_n records, holdout the next
+    cifar_paths: tuple = ()
 
 
 # MobileNetV2-CIFAR (width multiplier 0.5): the BASELINE.json configs[2]
@@ -236,10 +239,25 @@ def build_cnn_prediction_workload(cfg: CnnConfig | None = None) -> Workload:
     generic split upload applies."""
     cfg = cfg or CnnConfig()
     total = cfg.search_n + cfg.holdout_n
-    x, labels = cifar_synthetic(total, cfg.data_seed, cfg.side, cfg.in_channels, cfg.classes)
+    records = None
+    if cfg.cifar_paths:
+        from . import datasets as D
+        if (cfg.side, cfg.in_channels, cfg.classes) != (D.CIFAR_SIDE, D.CIFAR_CHANNELS, 10):
+            raise WorkloadError("CIFAR-10 records are 32x32x3 with 10 classes")
+        records = D.read_cifar_bin(cfg.cifar_paths)
+        if len(records) < total:
+            raise WorkloadError(f"dataset has {len(records)} examples, need {total}")
+        records = records[:total]
+        x, labels = D.cifar_records_to_nhwc(records)
+    else:
+        x, labels = cifar_synthetic(total, cfg.data_seed, cfg.side, cfg.in_channels,
+                                    cfg.classes)
     x = x.reshape(total, -1)
-    ds = Dataset(SplitView("search", x[:cfg.search_n], labels[:cfg.search_n]),
-                 SplitView("holdout", x[cfg.search_n:], labels[cfg.search_n:]),
+    cut = (lambda a, lo, hi: None if a is None else a[lo:hi])
+    ds = Dataset(SplitView("search", x[:cfg.search_n], labels[:cfg.search_n],
+                           records=cut(records, 0, cfg.search_n)),
+                 SplitView("holdout", x[cfg.search_n:total], labels[cfg.search_n:total],
+                           records=cut(records, cfg.search_n, total)),
                  x.shape[1], cfg.classes)
     text, flat = cnn_forward_text(cfg)
     module = parse_module(text)

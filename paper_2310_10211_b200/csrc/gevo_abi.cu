@@ -217,6 +217,108 @@ int gevo_upload_split(gevo_ctx* ctx, int split_id, const double* x, int64_t n,
   return GEVO_OK;
 }
 
+// a split's device arrays for nb whole batches (frees the previous ones)
+static int alloc_split(gevo_ctx* ctx, int split_id, int64_t n, int features, int classes,
+                       int batch, Split** out) {
+  Split& s = ctx->splits[split_id];
+  cudaFree(s.x);
+  cudaFree(s.y);
+  cudaFree(s.labels);
+  s = Split();
+  const int nb = (int)(n / batch);
+  const int64_t rows = (int64_t)nb * batch;
+  if (rows > 0) {
+    CK(cudaMalloc(&s.x, rows * features * sizeof(double)));
+    CK(cudaMalloc(&s.y, rows * classes * sizeof(double)));
+    CK(cudaMalloc(&s.labels, rows * sizeof(int64_t)));
+  }
+  s.nb = nb;
+  s.batch = batch;
+  s.features = features;
+  s.classes = classes;
+  *out = &s;
+  return GEVO_OK;
+}
+
+static int device_sms(gevo_ctx* ctx) {
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess)
+    sms = 148;
+  return sms;
+}
+
+int gevo_upload_split_u8(gevo_ctx* ctx, int split_id, const uint8_t* pixels, int64_t n,
+                         int features, const int64_t* labels, int classes, int batch) {
+  if (!ctx) return GEVO_E_ARG;
+  if (split_id < 0 || split_id >= 4 || !pixels || !labels || n < 0 || features <= 0 ||
+      classes <= 0 || batch <= 0)
+    return fail(ctx, GEVO_E_ARG, "bad split arguments");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t rows = (n / batch) * batch;
+  for (int64_t i = 0; i < rows; ++i)
+    if (labels[i] < 0 || labels[i] >= classes) return fail(ctx, GEVO_E_ARG, "label out of range");
+  Split* s = nullptr;
+  int rc = alloc_split(ctx, split_id, n, features, classes, batch, &s);
+  if (rc) return rc;
+  if (rows == 0) return GEVO_OK;
+  const int64_t count = rows * features;
+  uint8_t* raw = nullptr;
+  CK(cudaMalloc(&raw, count));
+  CK(cudaMemcpyAsync(raw, pixels, count, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(s->labels, labels, rows * sizeof(int64_t), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  const int sms = device_sms(ctx);
+  launch_decode_u8(raw, count, s->x, sms, ctx->stream);
+  launch_one_hot(s->labels, rows, classes, s->y, sms, ctx->stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(raw);
+  return GEVO_OK;
+}
+
+int gevo_upload_split_cifar(gevo_ctx* ctx, int split_id, const uint8_t* records, int64_t n,
+                            int channels, int side, int classes, int batch) {
+  if (!ctx) return GEVO_E_ARG;
+  if (split_id < 0 || split_id >= 4 || !records || n < 0 || channels <= 0 || side <= 0 ||
+      classes <= 0 || batch <= 0)
+    return fail(ctx, GEVO_E_ARG, "bad split arguments");
+  CK(cudaSetDevice(ctx->device));
+  const int HW = side * side;
+  const int64_t rec_bytes = 1 + (int64_t)channels * HW;
+  const int64_t rows = (n / batch) * batch;
+  for (int64_t i = 0; i < rows; ++i)
+    if (records[i * rec_bytes] >= classes) return fail(ctx, GEVO_E_ARG, "label out of range");
+  Split* s = nullptr;
+  int rc = alloc_split(ctx, split_id, n, channels * HW, classes, batch, &s);
+  if (rc) return rc;
+  if (rows == 0) return GEVO_OK;
+  uint8_t* raw = nullptr;
+  CK(cudaMalloc(&raw, rows * rec_bytes));
+  CK(cudaMemcpyAsync(raw, records, rows * rec_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  const int sms = device_sms(ctx);
+  launch_decode_cifar(raw, rows, channels, HW, s->x, s->labels, sms, ctx->stream);
+  launch_one_hot(s->labels, rows, classes, s->y, sms, ctx->stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(raw);
+  return GEVO_OK;
+}
+
+int gevo_download_split(gevo_ctx* ctx, int split_id, double* x, double* y, int64_t* labels,
+                        int64_t* rows) {
+  if (!ctx) return GEVO_E_ARG;
+  if (split_id < 0 || split_id >= 4 || !rows) return fail(ctx, GEVO_E_ARG, "bad split id");
+  CK(cudaSetDevice(ctx->device));
+  const Split& s = ctx->splits[split_id];
+  const int64_t r = (int64_t)s.nb * s.batch;
+  *rows = r;
+  if (r == 0) return GEVO_OK;
+  if (x) CK(cudaMemcpy(x, s.x, r * s.features * sizeof(double), cudaMemcpyDeviceToHost));
+  if (y) CK(cudaMemcpy(y, s.y, r * s.classes * sizeof(double), cudaMemcpyDeviceToHost));
+  if (labels) CK(cudaMemcpy(labels, s.labels, r * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return GEVO_OK;
+}
+
 int gevo_upload_weights(gevo_ctx* ctx, const double* w, int64_t n_elems) {
   if (!ctx) return GEVO_E_ARG;
   if (!w || n_elems <= 0) return fail(ctx, GEVO_E_ARG, "bad weights");

@@ -83,6 +83,13 @@ struct HvArgs {
 };
 
 void launch_archive_merge(const ArchArgs& a, cudaStream_t st);
+
+// dataset bytes -> split arrays (splits.cu)
+void launch_decode_u8(const uint8_t* px, int64_t count, double* x, int sms, cudaStream_t st);
+void launch_decode_cifar(const uint8_t* rec, int64_t rows, int C, int HW, double* x,
+                         int64_t* labels, int sms, cudaStream_t st);
+void launch_one_hot(const int64_t* labels, int64_t rows, int classes, double* y, int sms,
+                    cudaStream_t st);
 void launch_hypervolume(const HvArgs& a, cudaStream_t st);
 
 }  // namespace gevo

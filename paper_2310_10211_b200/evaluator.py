@@ -99,6 +99,27 @@ def lower_all(variants, cost_table, training, steps=600):
     return out
 
 
+def upload_split(ctx, split_id, split, classes, batch):
+    """Put a SplitView on the device (datasets.py:149-162 semantics).  Byte
+    sources cross as bytes and are decoded on the device: CIFAR records
+    (`split.records`), pixel bytes (`split.raw`), or the bytes recovered from
+    an exactly byte-scaled float64 x (evotir's own splits); anything else is
+    uploaded as float64."""
+    from . import datasets as D
+    records = getattr(split, "records", None)
+    if records is not None:
+        ctx.upload_split_cifar(split_id, records, D.CIFAR_CHANNELS, D.CIFAR_SIDE, classes, batch)
+        return "cifar"
+    raw = getattr(split, "raw", None)
+    if raw is None:
+        raw = D.pixel_bytes(split.x)
+    if raw is not None:
+        ctx.upload_split_u8(split_id, raw, split.labels, classes, batch)
+        return "u8"
+    ctx.upload_split(split_id, split.x, split.labels, classes, batch)
+    return "f64"
+
+
 class DeviceEvaluator:
     """Owns one device context with the workload's splits and weights
     resident; evaluates lists of variant programs.
@@ -114,8 +135,7 @@ class DeviceEvaluator:
         cfg = workload.config
         self.batch, self.classes = cfg.batch_size, cfg.classes
         ds = workload.dataset
-        self.ctx.upload_split(SPLIT_SEARCH, ds.search.x, ds.search.labels,
-                              cfg.classes, cfg.batch_size)
+        upload_split(self.ctx, SPLIT_SEARCH, ds.search, cfg.classes, cfg.batch_size)
         self.n_search_batches = len(ds.search.labels) // cfg.batch_size
         self._holdout_batches = None
         # weight arrays in parameter order (w1, b1, w2, b2 for 2fcNet; the
@@ -149,11 +169,9 @@ class DeviceEvaluator:
         if self._ctx2 is None:
             c = _lib.Context(self.device)
             ds, cfg = self.workload.dataset, self.workload.config
-            c.upload_split(SPLIT_SEARCH, ds.search.x, ds.search.labels, cfg.classes,
-                           cfg.batch_size)
+            upload_split(c, SPLIT_SEARCH, ds.search, cfg.classes, cfg.batch_size)
             if self._holdout_batches is not None:
-                c.upload_split(SPLIT_HOLDOUT, ds.holdout.x, ds.holdout.labels,
-                               cfg.classes, cfg.batch_size)
+                upload_split(c, SPLIT_HOLDOUT, ds.holdout, cfg.classes, cfg.batch_size)
             c.upload_weights(self._flat_weights)
             self._ctx2 = c
         return self._ctx2
@@ -164,8 +182,7 @@ class DeviceEvaluator:
             ds.holdout.reads += 1      # the only reader of holdout (fitness.py:404)
             for c in (self.ctx, self._ctx2):
                 if c is not None:
-                    c.upload_split(SPLIT_HOLDOUT, ds.holdout.x, ds.holdout.labels,
-                                   cfg.classes, cfg.batch_size)
+                    upload_split(c, SPLIT_HOLDOUT, ds.holdout, cfg.classes, cfg.batch_size)
             self._holdout_batches = len(ds.holdout.labels) // cfg.batch_size
         return self._holdout_batches
 

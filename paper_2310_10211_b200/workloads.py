@@ -8,7 +8,8 @@ against the reference and `tests/golden/*` carries the hashes.
 * `synthetic_digits`   <- datasets.py:88-109
 * `gaussian_blobs`     <- datasets.py:112-120
 * `SplitView.whole_batches` <- datasets.py:149-162 (stacked, not a list)
-* `DatasetConfig` / `load_dataset` <- datasets.py:173-229 (synthetic/blobs)
+* `DatasetConfig` / `load_dataset` <- datasets.py:173-229 (all four sources;
+  the byte readers are in datasets.py of this package)
 * `WorkloadConfig`     <- fitness.py:56-68
 * `init_weights`       <- fitness.py:218-227
 * `two_layer_program`  <- fitness.py:115-215 (same op sequence and names)
@@ -80,6 +81,11 @@ class SplitView:
     x: np.ndarray
     labels: np.ndarray
     reads: int = 0
+    # the pixel bytes x was scaled from (x == raw / 255.0), when the source
+    # had them: the device split is then uploaded as bytes and decoded there
+    raw: np.ndarray | None = None
+    # CIFAR-10 binary records x was decoded from (datasets.read_cifar_bin)
+    records: np.ndarray | None = None
 
     def __len__(self):
         return len(self.labels)
@@ -121,24 +127,52 @@ class DatasetConfig:
 
 
 def load_dataset(cfg: DatasetConfig) -> Dataset:
+    """datasets.py:187-229: synthetic, blobs, idx (train/t10k, optional .gz)
+    and csv sources; the same checks and the same float64 x.  Byte sources
+    keep their pixels in `SplitView.raw` for the device upload."""
+    from . import datasets as D
     total = cfg.search_n + cfg.holdout_n
+    raw = None
     if cfg.source == "synthetic":
         side = int(round(cfg.features ** 0.5))
         if side * side != cfg.features:
-            raise WorkloadError("synthetic digits need a square feature count")
+            raise D.DatasetError("synthetic digits need a square feature count")
         img, labels = synthetic_digits(total, cfg.data_seed, cfg.noise,
                                        cfg.separation, cfg.classes, side)
-        x = img.reshape(total, -1).astype(np.float64) / 255.0
+        raw = img.reshape(total, -1)
     elif cfg.source == "blobs":
-        if cfg.classes != 2:
-            raise WorkloadError("blobs is a two-class dataset")
         x, labels = gaussian_blobs(total, cfg.data_seed, cfg.features)
+        if cfg.classes != 2:
+            raise D.DatasetError("blobs is a two-class dataset")
+    elif cfg.source == "idx":
+        if not cfg.directory:
+            raise D.DatasetError("idx source needs a dataset directory")
+        images_path = D.find_idx_file(cfg.directory, "images-idx3-ubyte")
+        labels_path = D.find_idx_file(cfg.directory, "labels-idx1-ubyte")
+        raw = D.read_idx_images(images_path)
+        labels = D.read_idx_labels(labels_path)
+    elif cfg.source == "csv":
+        if not cfg.csv_path:
+            raise D.DatasetError("csv source needs csv_path")
+        vals, labels = D.read_csv_dataset(cfg.csv_path)
+        if vals.dtype == np.uint8:
+            raw = vals
+        else:
+            x = vals / 255.0
     else:
-        raise WorkloadError(f"dataset source {cfg.source!r} not supported "
-                            "by the device evaluator")
-    return Dataset(SplitView("search", x[:cfg.search_n], labels[:cfg.search_n]),
-                   SplitView("holdout", x[cfg.search_n:total],
-                             labels[cfg.search_n:total]),
+        raise D.DatasetError(f"unknown dataset source {cfg.source!r}")
+    if raw is not None:
+        x = raw.astype(np.float64) / 255.0
+    if len(labels) < total:
+        raise D.DatasetError(f"dataset has {len(labels)} examples, need {total} "
+                             f"(search {cfg.search_n} + holdout {cfg.holdout_n})")
+    if x.shape[1] != cfg.features:
+        raise D.DatasetError(f"dataset has {x.shape[1]} features, expected {cfg.features}")
+    cut = (lambda a, lo, hi: None if a is None else a[lo:hi])
+    return Dataset(SplitView("search", x[:cfg.search_n], labels[:cfg.search_n],
+                             raw=cut(raw, 0, cfg.search_n)),
+                   SplitView("holdout", x[cfg.search_n:total], labels[cfg.search_n:total],
+                             raw=cut(raw, cfg.search_n, total)),
                    cfg.features, cfg.classes)
 
 

@@ -21,6 +21,8 @@ class FakeContext:
     def upload_split(self, *a):
         pass
 
+    upload_split_u8 = upload_split_cifar = upload_split
+
     def num_sms(self):
         return 148
 
