@@ -222,7 +222,23 @@ struct DotArgs {
   double* out;
   int som, son;
   int M, K;
+  int xrow;     // ACC8 outputs in rows >= xrow reduce their lanes in the
+                // AVX-512 order (OpenBLAS edge kernels for the m % 4 rows)
 };
+
+// the 8 lane chains of output h (lane j in acc[2j + h]) folded to one value:
+// the pairwise tree ((0+1)+(2+3))+((4+5)+(6+7)) of the full-width kernels, or
+// (avx) the _mm512_reduce_add_pd order ((0+4)+(2+6))+((1+5)+(3+7)) of the
+// OpenBLAS edge kernels (lowering.dot_modes)
+__device__ __forceinline__ double lane_tree(const double* acc, int h, bool avx) {
+  const double l0 = acc[h], l1 = acc[2 + h], l2 = acc[4 + h], l3 = acc[6 + h];
+  const double l4 = acc[8 + h], l5 = acc[10 + h], l6 = acc[12 + h], l7 = acc[14 + h];
+  if (avx)
+    return __dadd_rn(__dadd_rn(__dadd_rn(l0, l4), __dadd_rn(l2, l6)),
+                     __dadd_rn(__dadd_rn(l1, l5), __dadd_rn(l3, l7)));
+  return __dadd_rn(__dadd_rn(__dadd_rn(l0, l1), __dadd_rn(l2, l3)),
+                   __dadd_rn(__dadd_rn(l4, l5), __dadd_rn(l6, l7)));
+}
 
 // Panel epilogue + store (all threads): the panel's raw dot values sit in
 // the C tile (row-major, stride kCS); thread t handles elements
@@ -496,10 +512,9 @@ __device__ __forceinline__ void dot_pipeline(const DotArgs& dref, int col0, int 
           }
         }
         if (last) {
-          r0 = __dadd_rn(__dadd_rn(__dadd_rn(acc[0], acc[2]), __dadd_rn(acc[4], acc[6])),
-                         __dadd_rn(__dadd_rn(acc[8], acc[10]), __dadd_rn(acc[12], acc[14])));
-          r1 = __dadd_rn(__dadd_rn(__dadd_rn(acc[1], acc[3]), __dadd_rn(acc[5], acc[7])),
-                         __dadd_rn(__dadd_rn(acc[9], acc[11]), __dadd_rn(acc[13], acc[15])));
+          const bool avx = m0 + lm >= d.xrow;
+          r0 = lane_tree(acc, 0, avx);
+          r1 = lane_tree(acc, 1, avx);
 #pragma unroll 1
           for (int kk = kmain - k0; kk < nk; ++kk) {     // ACC8_TAIL: k >= K&~7
             const int pk = ((kk & 7) << 2) | (kk >> 3);
@@ -1276,10 +1291,9 @@ __device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, d
       }
       if (last) {
         // pairwise lane tree, then (ACC8_TAIL) the fma tail over k >= K&~7
-        double r0 = __dadd_rn(__dadd_rn(__dadd_rn(acc[0], acc[2]), __dadd_rn(acc[4], acc[6])),
-                              __dadd_rn(__dadd_rn(acc[8], acc[10]), __dadd_rn(acc[12], acc[14])));
-        double r1 = __dadd_rn(__dadd_rn(__dadd_rn(acc[1], acc[3]), __dadd_rn(acc[5], acc[7])),
-                              __dadd_rn(__dadd_rn(acc[9], acc[11]), __dadd_rn(acc[13], acc[15])));
+        const bool avx = (PANELS ? s * kPanel : 0) + lm >= d.xrow;
+        double r0 = lane_tree(acc, 0, avx);
+        double r1 = lane_tree(acc, 1, avx);
 #pragma unroll 1
         for (int kk = kmain - k0; kk < nk; ++kk) {
           const double a = As[lm * ars + kk * aks];
@@ -1440,8 +1454,7 @@ __device__ __noinline__ void dot_tiny(const DotArgs& dref, int col0, int col1, c
     double r[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      r[h] = __dadd_rn(__dadd_rn(__dadd_rn(acc[h], acc[2 + h]), __dadd_rn(acc[4 + h], acc[6 + h])),
-                       __dadd_rn(__dadd_rn(acc[8 + h], acc[10 + h]), __dadd_rn(acc[12 + h], acc[14 + h])));
+      r[h] = lane_tree(acc, h, m >= d.xrow);
       const int nn = cb0 * 8 + 2 * t4 + h;
       for (int k = kmain; k < K; ++k)                  // ACC8_TAIL
         if (nn < ncols)

@@ -502,7 +502,10 @@ __device__ __noinline__ void run_dot(Shared& S, const gevo_instr& I, double* sta
   const int N = I.shp[1];
   const bool integer = I.kin != GEVO_K_F64;
   const int split = integer ? N : min(I.aux[1], N);
+  d.xrow = 1 << 30;
   dot_columns(d, 0, split, I.sub, integer, stage, epi);
+  // aux[3] = 1 + first row of the edge corner (0: none), columns >= split
+  if (I.aux[3] > 0) d.xrow = I.aux[3] - 1;
   dot_columns(d, split, N, I.aux[2], integer, stage, epi);
 }
 

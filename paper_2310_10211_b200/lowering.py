@@ -120,31 +120,47 @@ def _blas2d(s_outer, s_inner, d_inner) -> bool:
     return s_inner == 1 and s_outer >= d_inner
 
 
+def _blas_strides(st, rows, cols):
+    """The strides numpy's BLAS call sees for a 2-D operand.  A blasable
+    operand (numpy is_blasable2d in either orientation) is passed as is; any
+    other -- in this dialect, a broadcast view with a zero stride -- is first
+    copied in KEEPORDER: C order unless axis 1 has the larger stride (ties,
+    e.g. a broadcast scalar, stay C).  Probed on numpy 2.3.5: every
+    broadcast/transposed combination reproduces this (profiles/
+    r01_dot_orders.md); the no-FMA loop is never taken for these shapes."""
+    if _blas2d(st[0], st[1], cols) or _blas2d(st[1], st[0], rows):
+        return st
+    return (1, rows) if abs(st[1]) > abs(st[0]) else (cols, 1)
+
+
 def dot_modes(a: Val, b: Val):
-    """(mode for columns < split, split, mode for the rest) reproducing the
-    summation order numpy `@` + OpenBLAS (SkylakeX kernels, the build
-    container's numpy 2.3 / OpenBLAS 0.3.30) use; see DESIGN.md."""
+    """(mode for columns < split, split, mode for the rest, xrow) reproducing
+    the summation order numpy `@` + OpenBLAS (SkylakeX kernels, the build
+    container's numpy 2.3 / OpenBLAS 0.3.30) use; see DESIGN.md.  In the
+    columns >= split, ACC8 outputs of rows >= xrow (the m % 4 rows of the edge
+    kernels) reduce their 8 lanes in the AVX-512 order instead of the
+    pairwise tree; xrow = m when there is no such corner."""
     m, k = a.shape
     n = b.shape[1]
     if a.kind != K_F64:
-        return D_SEQ_NOFMA, n, D_SEQ_NOFMA       # integer: exact anyway
-    a_c = _blas2d(a.st[0], a.st[1], k)
-    a_f = _blas2d(a.st[1], a.st[0], m)
-    b_c = _blas2d(b.st[0], b.st[1], n)
-    b_f = _blas2d(b.st[1], b.st[0], k)
-    if not ((a_c or a_f) and (b_c or b_f)):
-        return D_SEQ_NOFMA, n, D_SEQ_NOFMA       # numpy's own loop
+        return D_SEQ_NOFMA, n, D_SEQ_NOFMA, m    # integer: exact anyway
+    sa = _blas_strides(a.st, m, k)
+    sb = _blas_strides(b.st, k, n)
+    a_c = _blas2d(sa[0], sa[1], k)
+    b_c = _blas2d(sb[0], sb[1], n)
     if m == 1 or k == 1 or n == 1:
-        return D_FMA_CHAIN, n, D_FMA_CHAIN       # gemv/dot paths (see DESIGN)
+        return D_FMA_CHAIN, n, D_FMA_CHAIN, m    # gemv/dot paths (see DESIGN)
     trans_a, trans_b = not a_c, not b_c
+    corner = m - m % 4 if n % 8 and m % 4 else m
     # cblas row-major -> col-major: A' = B (trans_b), B' = A (trans_a)
     tn = trans_b and not trans_a
     small = m * n * k <= 1_000_000 and (not tn or (m * n <= 1200 and k >= 32))
     if small and tn:
-        return D_ACC8_TREE, n, D_ACC8_TREE
-    if not trans_a and not trans_b and n % 8:
-        return D_FMA_CHAIN, n - n % 8, D_ACC8_TREE
-    return D_FMA_CHAIN, n, D_FMA_CHAIN
+        return D_ACC8_TREE, n - n % 8, D_ACC8_TREE, corner
+    if not trans_a and not trans_b and n % 8 and k >= 16:
+        # the n % 8 edge columns of the NN kernel: 8 lane chains once K >= 16
+        return D_FMA_CHAIN, n - n % 8, D_ACC8_TREE, corner
+    return D_FMA_CHAIN, n, D_FMA_CHAIN, m
 
 
 def _pad_dims(shape):
@@ -321,8 +337,9 @@ class _Builder:
         if code == "dot":
             a, b = ins
             out = self.result_val(op, shape, L.c_strides(shape), kind)
-            m1, split, m2 = dot_modes(a, b)
-            self.emit(OP_DOT, m1, out, ins, aux=[a.shape[1], split, m2])
+            m1, split, m2, xrow = dot_modes(a, b)
+            corner = xrow + 1 if xrow < a.shape[0] else 0
+            self.emit(OP_DOT, m1, out, ins, aux=[a.shape[1], split, m2, corner])
             return out
         if code == "reduce":
             (a,) = ins

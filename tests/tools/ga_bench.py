@@ -28,9 +28,13 @@ from golden_io import load  # noqa: E402
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
-    name = args[0] if args else "ga512x50.json.gz"
-    out_path = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    argv = sys.argv[1:]
+    out_path = None
+    if "--out" in argv:
+        k = argv.index("--out")
+        out_path = argv[k + 1]
+        del argv[k:k + 2]
+    name = argv[0] if argv else "ga512x50.json.gz"
     from paper_2310_10211_b200 import workloads
     from paper_2310_10211_b200.evaluator import DeviceEvaluator
     data = load(name)
