@@ -473,6 +473,44 @@ __device__ __forceinline__ double epilogue(const EpiDev& e, const double* ev, do
   return epilogue_generic(e, ev, v, r, c);
 }
 
+// An elementwise instruction with a fused chain (lowering.fuse_ew_chains):
+// the instruction's own op, then the decoded micro-ops on each element, one
+// store.  rank <= 2; element i = (r, c) of the output, operands addressed by
+// their (r, c) strides (rank 1: one row).  EXT records follow the
+// instruction (aux2[4] of them, aux2[5] micro-ops).
+__device__ __noinline__ void run_ew_chain(Shared& S, const gevo_instr& I) {
+  if (threadIdx.x == 0) decode_epilogue(S, &I + 1, I.aux2[4], I.aux2[5]);
+  __syncthreads();
+  const EpiDev& e = S.epi;
+  const int n = I.n, rank = I.rank, op = I.op, sub = I.sub, kin = I.kin, kout = I.kout;
+  const int C = rank == 2 ? I.shp[1] : (rank == 1 ? I.shp[0] : 1);
+  const gevo_operand* ops[4] = {&I.out, &I.in[0], &I.in[1], &I.in[2]};
+  const int nin = op == GEVO_OP_UNARY ? 1 : (op == GEVO_OP_BINARY ? 2 : 3);
+  double* p[4];
+  int s0[4], s1[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const gevo_operand& o = *ops[k];
+    const bool used = k <= nin;
+    p[k] = used ? S.base[o.buf] + o.off : S.base[0];
+    s0[k] = used && rank == 2 ? o.st[0] : 0;
+    s1[k] = used ? (rank == 2 ? o.st[1] : (rank == 1 ? o.st[0] : 0)) : 0;
+  }
+  for (int i = threadIdx.x; i < n; i += kThreads) {
+    const int r = i / C, c = i - r * C;
+    const double a = p[1][r * s0[1] + c * s1[1]];
+    const double b = nin > 1 ? p[2][r * s0[2] + c * s1[2]] : 0.0;
+    const double x = nin > 2 ? p[3][r * s0[3] + c * s1[3]] : 0.0;
+    double v;
+    if (op == GEVO_OP_UNARY) v = apply_unary(sub, kin, kout, a);
+    else if (op == GEVO_OP_BINARY) v = apply_binary(sub, kin, a, b);
+    else v = as_i64(a) != 0 ? b : x;
+    double ev[kEpiPre];
+    epi_fetch(e, r, c, ev);
+    p[0][r * s0[0] + c * s1[0]] = epilogue(e, ev, v, r, c);
+  }
+}
+
 }  // namespace gevo
 #include "dot_staged.cuh"
 namespace gevo {
@@ -524,7 +562,8 @@ __device__ __noinline__ void run_instrs(Shared& S, const gevo_instr* ins, int n,
     // small f64 binary ops with linear/scalar operands (most of a step's
     // non-dot instructions): inline, no call
     if (I.op == GEVO_OP_BINARY && I.kin == GEVO_K_F64 && I.sub <= GEVO_B_MAX && I.n <= 2 * kThreads &&
-        I.aux2[0] != AM_STRIDED && I.aux2[1] != AM_STRIDED && I.aux2[2] != AM_STRIDED) {
+        I.aux2[0] != AM_STRIDED && I.aux2[1] != AM_STRIDED && I.aux2[2] != AM_STRIDED &&
+        I.aux2[4] == 0) {
       const int n_ = I.n, sub = I.sub;
       const int so = I.aux2[0] == AM_LINEAR, sa = I.aux2[1] == AM_LINEAR, sb = I.aux2[2] == AM_LINEAR;
       double* o = S.base[I.out.buf] + I.out.off;
@@ -548,7 +587,14 @@ __device__ __noinline__ void run_instrs(Shared& S, const gevo_instr* ins, int n,
     } else switch (I.op) {
       case GEVO_OP_UNARY:
       case GEVO_OP_BINARY:
-      case GEVO_OP_SELECT: run_elementwise(S, I); break;
+      case GEVO_OP_SELECT:
+        if (I.aux2[4] > 0) {
+          run_ew_chain(S, I);
+          k += I.aux2[4];
+        } else {
+          run_elementwise(S, I);
+        }
+        break;
       case GEVO_OP_REDUCE: run_reduce(S, I); break;
       case GEVO_OP_DOT: run_dot(S, I, stage); k += I.aux2[0]; break;
       case GEVO_OP_PAD: run_pad(S, I); break;

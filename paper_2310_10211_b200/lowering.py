@@ -528,6 +528,97 @@ def fuse_dot_epilogues(instrs):
             del instrs[i]
 
 
+_EW_OPS = (OP_UNARY, OP_BINARY, OP_SELECT)
+
+
+def _as2d(v: Val) -> Val:
+    """An epilogue operand as a (rows, cols) view: epilogue operands are
+    addressed by (r, c) with two strides; rank 1 is one row, rank 0 one
+    element."""
+    if len(v.shape) == 2:
+        return v
+    if len(v.shape) == 1:
+        return Val(v.buf, v.off, (1, v.shape[0]), (0, v.st[0]), v.kind, v.alloc)
+    return Val(v.buf, v.off, (1, 1), (0, 0), v.kind, v.alloc)
+
+
+def fuse_ew_chains(instrs):
+    """Fold a single-use elementwise result into its elementwise consumer.
+
+    Like fuse_dot_epilogues, with an elementwise producer P (rank <= 2) in
+    place of the dot: P's result lives in scratch and is read exactly once,
+    through the identity view, by an elementwise R of the same shape.  P's
+    op stays the instruction's own op, R becomes an epilogue micro-op on it,
+    and the fused instruction takes R's place; P's value is never stored.
+    e.g. b1' = b1 - lr * g is one instruction, and so is exp(z - max).  Each
+    micro-op rounds like the instruction it replaces (bit-identical)."""
+    while True:
+        readers = {}
+        for i, r in enumerate(instrs):
+            for k, v in enumerate(r["in"]):
+                if v.alloc >= 0:
+                    readers.setdefault(v.alloc, []).append((i, k, "in"))
+            for k, v in enumerate(r.get("ext", [])):
+                if v.alloc >= 0:
+                    readers.setdefault(v.alloc, []).append((i, k, "ext"))
+        touched, drop = set(), []
+        for i, p in enumerate(instrs):
+            if p["op"] not in _EW_OPS or i in touched:
+                continue
+            out = p["out"]
+            if out.alloc < 0 or out.buf != BUF_ARENA or len(out.shape) > 2:
+                continue
+            rs = readers.get(out.alloc, [])
+            if len(rs) != 1 or rs[0][2] != "in":
+                continue
+            j, k, _ = rs[0]
+            r = instrs[j]
+            if j <= i or j in touched or r["op"] not in _EW_OPS:
+                continue
+            if not _same_view(r["in"][k], out) or tuple(r["out"].shape) != tuple(out.shape):
+                continue
+            epi = list(p.get("epi", []))
+            ext = list(p.get("ext", []))
+            others = [w for kk, w in enumerate(r["in"]) if kk != k]
+            r_epi, r_ext = r.get("epi", []), r.get("ext", [])
+            if len(epi) + 1 + len(r_epi) > EPI_MAX_OPS or \
+                    len(ext) + len(others) + len(r_ext) > EPI_MAX_EXT:
+                continue
+            prev = 0 if not epi else EPI_SRC_OP + len(epi) - 1
+            srcs = []
+            for kk, w in enumerate(r["in"]):
+                if kk == k:
+                    srcs.append(prev)
+                else:
+                    ext.append(_as2d(w))
+                    srcs.append(len(ext))    # 1-based operand index
+            epi.append((r["op"], r["sub"], r["kin"], r["kout"], srcs))
+            # R's own chain (from an earlier merge) follows, re-indexed: its
+            # value -> the micro-op just added, its micro-ops and operands
+            # shifted past P's
+            r_op_at, ext0 = EPI_SRC_OP + len(epi) - 1, len(ext)
+            for cls, sub, kin, kout, rs_ in r_epi:
+                m = []
+                for x in rs_:
+                    if x == 0:
+                        m.append(r_op_at)
+                    elif x >= EPI_SRC_OP:
+                        m.append(r_op_at + 1 + (x - EPI_SRC_OP))
+                    else:
+                        m.append(ext0 + x)
+                epi.append((cls, sub, kin, kout, m))
+            ext.extend(r_ext)
+            new = dict(p)
+            new["epi"], new["ext"], new["out"] = epi, ext, r["out"]
+            instrs[j] = new
+            drop.append(i)
+            touched.update((i, j))
+        if not drop:
+            return instrs
+        for i in reversed(drop):
+            del instrs[i]
+
+
 def lower_function(fn, param_layouts=None, ret_bufs=None, ret_layout="compact",
                    cost_table=None, smem_budget=None, fuse=True) -> Lowered:
     """Lower one function.  Params i live in buffer PARAM0+i with the given
@@ -544,6 +635,7 @@ def lower_function(fn, param_layouts=None, ret_bufs=None, ret_layout="compact",
     ret_st = b.run(fn.returns)
     if fuse:
         fuse_dot_epilogues(b.instrs)
+        fuse_ew_chains(b.instrs)
     top, stop = b.assign_arena(smem_budget)
     # resolve arena offsets into the operands
     instrs = []
@@ -612,12 +704,14 @@ def encode_instrs(instrs, const_base=0) -> np.ndarray:
     words = []
     for rec in instrs:
         recs = [rec]
+        n_ext = n_epi = 0
         if rec.get("epi"):
             exts = _ext_records(rec)
+            n_ext, n_epi = len(exts), len(rec["epi"])
             rec = dict(rec)
             aux2 = list(rec["aux2"])
-            aux2[0] = len(exts)
-            aux2[1] = len(rec["epi"])
+            aux2[0] = n_ext          # DOT: aux2[0..1]; elementwise: aux2[4..5]
+            aux2[1] = n_epi
             rec["aux2"] = aux2
             recs = [rec] + exts
         for r in recs:
@@ -627,7 +721,7 @@ def encode_instrs(instrs, const_base=0) -> np.ndarray:
                 shape = tuple(r["out"].shape)
                 modes = [_addr_mode(r["out"], shape)]
                 modes += [_addr_mode(v, shape) for v in ins]
-                aux2 = modes + [AM_SCALAR] * (4 - len(modes)) + [0] * (MAXR - 4)
+                aux2 = modes + [AM_SCALAR] * (4 - len(modes)) + [n_ext, n_epi]
             words += [r["op"], r["sub"], r["kout"], r["kin"], r["rank"], r["n"]]
             words += r["shp"]
             words += r["aux"]

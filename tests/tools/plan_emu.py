@@ -74,6 +74,25 @@ def ew(op, sub, kin, kout, args):
         return [a == b, a != b, a < b, a <= b, a > b, a >= b][sub - 5].astype(np.int64)
 
 
+def apply_epilogue(mem, rec, r):
+    """Fused micro-ops (dot epilogues and elementwise chains) on the
+    instruction's own result r (flat, output order)."""
+    ext = [gather(mem, v, tuple(v.shape)).reshape(-1) for v in rec["ext"]]
+    vals = [r]
+    for cls, esub, ekin, ekout, srcs in rec["epi"]:
+        nin = {Lw.OP_UNARY: 1, Lw.OP_BINARY: 2, Lw.OP_SELECT: 3}[cls]
+        args = []
+        for s in srcs[:nin]:
+            if s == 0:
+                args.append(vals[0])
+            elif s >= Lw.EPI_SRC_OP:
+                args.append(vals[1 + s - Lw.EPI_SRC_OP])
+            else:
+                args.append(ext[s - 1])
+        vals.append(ew(cls, esub, ekin, ekout, args))
+    return vals[-1]
+
+
 def run(instrs, mem):
     """mem: dict buf_id -> np.ndarray of int64 words (float64 bits)."""
     for rec in instrs:
@@ -84,6 +103,8 @@ def run(instrs, mem):
         with np.errstate(all="ignore"):
             if op in (Lw.OP_UNARY, Lw.OP_BINARY, Lw.OP_SELECT):
                 r = ew(op, sub, kin, rec["kout"], [gather(mem, v, shape) for v in rec["in"]])
+                if rec.get("epi"):
+                    r = apply_epilogue(mem, rec, r)
             elif op == Lw.OP_REDUCE:
                 L, rs = rec["aux"][0], rec["aux"][1]
                 base = offsets(rec["in"][0], shape)
@@ -101,20 +122,7 @@ def run(instrs, mem):
                 B = gather(mem, b, (K, N)).reshape(K, N)
                 r = (wd(fl(A) @ fl(B)) if kin == F else A @ B).reshape(-1)
                 if rec.get("epi"):
-                    ext = [gather(mem, v, shape) for v in rec["ext"]]
-                    vals = [r]
-                    for cls, esub, ekin, ekout, srcs in rec["epi"]:
-                        nin = {Lw.OP_UNARY: 1, Lw.OP_BINARY: 2, Lw.OP_SELECT: 3}[cls]
-                        args = []
-                        for s in srcs[:nin]:
-                            if s == 0:
-                                args.append(vals[0])
-                            elif s >= Lw.EPI_SRC_OP:
-                                args.append(vals[1 + s - Lw.EPI_SRC_OP])
-                            else:
-                                args.append(ext[s - 1])
-                        vals.append(ew(cls, esub, ekin, ekout, args))
-                    r = vals[-1]
+                    r = apply_epilogue(mem, rec, r)
             elif op == Lw.OP_PAD:
                 a, pv = rec["in"]
                 low, ext_ = rec["aux"][:len(shape)], rec["aux2"][:len(shape)]
