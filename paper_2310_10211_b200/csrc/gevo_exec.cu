@@ -478,7 +478,57 @@ __device__ __forceinline__ double epilogue(const EpiDev& e, const double* ev, do
 // store.  rank <= 2; element i = (r, c) of the output, operands addressed by
 // their (r, c) strides (rank 1: one row).  EXT records follow the
 // instruction (aux2[4] of them, aux2[5] micro-ops).
+// fast form: an f64 binary op followed by <= 2 f64 binary micro-ops, micro-op
+// m combining the running value with EXT operand m + 1 (b1 - lr * g and the
+// like).  Every thread decodes the one EXT record into registers: no
+// shared-memory decode, no extra barrier.  Returns false for any other chain.
+__device__ __forceinline__ bool ew_chain_fast(const Shared& S, const gevo_instr& I) {
+  const int nops = I.aux2[5];
+  if (I.op != GEVO_OP_BINARY || I.kin != GEVO_K_F64 || I.sub > GEVO_B_MAX || nops > 2)
+    return false;
+  const gevo_instr& X = (&I)[1];
+  int fsub[2] = {0, 0}, fleft[2] = {0, 0};
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    if (m >= nops) break;
+    const int w0 = X.aux[3 * m], w1 = X.aux[3 * m + 1];
+    const int cls = w0 & 15, sub = (w0 >> 4) & 15, kin = (w0 >> 8) & 15;
+    const int s0 = w1 & 255, s1 = (w1 >> 8) & 255;
+    const int prev = m == 0 ? 0 : GEVO_EPI_SRC_OP + m - 1;
+    if (cls != GEVO_OP_BINARY || kin != GEVO_K_F64 || sub > GEVO_B_MAX) return false;
+    if (s0 == prev && s1 == m + 1) fleft[m] = 1;
+    else if (s1 == prev && s0 == m + 1) fleft[m] = 0;
+    else return false;
+    fsub[m] = sub;
+  }
+  const int n = I.n, rank = I.rank, sub = I.sub;
+  const int C = rank == 2 ? I.shp[1] : (rank == 1 ? I.shp[0] : 1);
+  auto st0 = [&](const gevo_operand& o) { return rank == 2 ? o.st[0] : 0; };
+  auto st1 = [&](const gevo_operand& o) { return rank == 2 ? o.st[1] : (rank == 1 ? o.st[0] : 0); };
+  double* out = S.base[I.out.buf] + I.out.off;
+  const double* a = S.base[I.in[0].buf] + I.in[0].off;
+  const double* b = S.base[I.in[1].buf] + I.in[1].off;
+  const int o0 = st0(I.out), o1 = st1(I.out), a0 = st0(I.in[0]), a1 = st1(I.in[0]);
+  const int b0 = st0(I.in[1]), b1 = st1(I.in[1]);
+  // EXT operands are (r, c) views already (lowering._as2d)
+  const double* e0 = S.base[X.in[0].buf] + X.in[0].off;
+  const double* e1 = nops > 1 ? S.base[X.in[1].buf] + X.in[1].off : e0;
+  const int e00 = X.in[0].st[0], e01 = X.in[0].st[1];
+  const int e10 = nops > 1 ? X.in[1].st[0] : 0, e11 = nops > 1 ? X.in[1].st[1] : 0;
+  for (int i = threadIdx.x; i < n; i += kThreads) {
+    const int r = i / C, c = i - r * C;
+    const double x0 = e0[r * e00 + c * e01];
+    const double x1 = nops > 1 ? e1[r * e10 + c * e11] : 0.0;
+    double v = bin_f64(sub, a[r * a0 + c * a1], b[r * b0 + c * b1]);
+    v = fleft[0] ? bin_f64(fsub[0], v, x0) : bin_f64(fsub[0], x0, v);
+    if (nops > 1) v = fleft[1] ? bin_f64(fsub[1], v, x1) : bin_f64(fsub[1], x1, v);
+    out[r * o0 + c * o1] = v;
+  }
+  return true;
+}
+
 __device__ __noinline__ void run_ew_chain(Shared& S, const gevo_instr& I) {
+  if (ew_chain_fast(S, I)) return;
   if (threadIdx.x == 0) decode_epilogue(S, &I + 1, I.aux2[4], I.aux2[5]);
   __syncthreads();
   const EpiDev& e = S.epi;

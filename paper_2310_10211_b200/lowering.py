@@ -529,6 +529,7 @@ def fuse_dot_epilogues(instrs):
 
 
 _EW_OPS = (OP_UNARY, OP_BINARY, OP_SELECT)
+EW_CHAIN_MAX = 2048    # larger tensors keep the 4-in-flight elementwise loops
 
 
 def _as2d(v: Val) -> Val:
@@ -566,7 +567,8 @@ def fuse_ew_chains(instrs):
             if p["op"] not in _EW_OPS or i in touched:
                 continue
             out = p["out"]
-            if out.alloc < 0 or out.buf != BUF_ARENA or len(out.shape) > 2:
+            if out.alloc < 0 or out.buf != BUF_ARENA or len(out.shape) > 2 or \
+                    math.prod(out.shape) > EW_CHAIN_MAX:
                 continue
             rs = readers.get(out.alloc, [])
             if len(rs) != 1 or rs[0][2] != "in":
