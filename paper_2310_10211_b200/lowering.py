@@ -23,6 +23,7 @@ order, so it is bit-identical.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -529,7 +530,8 @@ def fuse_dot_epilogues(instrs):
 
 
 _EW_OPS = (OP_UNARY, OP_BINARY, OP_SELECT)
-EW_CHAIN_MAX = 2048    # larger tensors keep the 4-in-flight elementwise loops
+# largest elementwise chain (elements); measured best without a limit
+EW_CHAIN_MAX = int(os.environ.get("GEVO_EW_CHAIN_MAX", 1 << 30))
 
 
 def _as2d(v: Val) -> Val:
