@@ -292,6 +292,59 @@ __device__ __noinline__ void run_pad(const Shared& S, const gevo_instr& I) {
   }
 }
 
+__device__ __noinline__ void run_reduce(const Shared& S, const gevo_instr& I) {
+  double* out = opptr(S, I.out);
+  const double* in = opptr(S, I.in[0]);
+  // the record's fields into registers (stores may alias it)
+  const int L = I.aux[0], n = I.n, rank = I.rank, kin = I.kin, sub = I.sub;
+  const int64_t rs = I.aux[1];
+  int shp[GEVO_MAXR], ist[GEVO_MAXR], ost[GEVO_MAXR];
+#pragma unroll
+  for (int d = 0; d < GEVO_MAXR; ++d) {
+    shp[d] = I.shp[d];
+    ist[d] = I.in[0].st[d];
+    ost[d] = I.out.st[d];
+  }
+  const int ioff = I.in[0].off, ooff = I.out.off;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int idx[GEVO_MAXR];
+    unravel(i, rank, shp, idx);
+    int src = ioff, dst = ooff;
+#pragma unroll
+    for (int d = 0; d < GEVO_MAXR; ++d) {
+      if (d < rank) {
+        src += idx[d] * ist[d];
+        dst += idx[d] * ost[d];
+      }
+    }
+    const double* p = in + src;
+    double r;
+    if (kin == GEVO_K_F64) {
+      if (sub == GEVO_R_MAX) {
+        r = p[0];
+        for (int k = 1; k < L; ++k) r = np_fmax(r, p[k * rs]);
+      } else if (sub == GEVO_R_SUM_PAIRWISE) {
+        r = pairwise_sum(p, L, rs);
+      } else {
+        r = 0.0;
+        for (int k = 0; k < L; ++k) r = __dadd_rn(r, p[k * rs]);
+      }
+    } else {
+      int64_t v;
+      if (sub == GEVO_R_MAX) {
+        v = as_i64(p[0]);
+        for (int k = 1; k < L; ++k) { int64_t x = as_i64(p[k * rs]); v = x > v ? x : v; }
+      } else {
+        uint64_t acc = 0;
+        for (int k = 0; k < L; ++k) acc += (uint64_t)as_i64(p[k * rs]);
+        v = (int64_t)acc;
+      }
+      r = as_w(v);
+    }
+    out[dst] = r;
+  }
+}
+
 // fused dot epilogues (the DOT itself: dot_staged.cuh)
 
 // decode the EXT records following a DOT (thread 0; caller syncs)
@@ -425,60 +478,29 @@ __device__ __forceinline__ double epilogue(const EpiDev& e, const double* ev, do
 // store.  rank <= 2; element i = (r, c) of the output, operands addressed by
 // their (r, c) strides (rank 1: one row).  EXT records follow the
 // instruction (aux2[4] of them, aux2[5] micro-ops).
-// A chain of <= 2 f64 binary micro-ops, micro-op m combining the running
-// value with EXT operand m + 1 (b1 - lr * g and the like), decoded by every
-// thread from the one EXT record into registers: no shared-memory decode, no
-// extra barrier.
-struct FastChain {
-  int nops, fsub[2], fleft[2];
-  const double* e[2];
-  int s0[2], s1[2];
-};
-
-__device__ __forceinline__ bool fast_chain(const Shared& S, const gevo_instr* X, int nops,
-                                           FastChain& f) {
-  if (nops > 2) return false;
-  f.nops = nops;
+// fast form: an f64 binary op followed by <= 2 f64 binary micro-ops, micro-op
+// m combining the running value with EXT operand m + 1 (b1 - lr * g and the
+// like).  Every thread decodes the one EXT record into registers: no
+// shared-memory decode, no extra barrier.  Returns false for any other chain.
+__device__ __forceinline__ bool ew_chain_fast(const Shared& S, const gevo_instr& I) {
+  const int nops = I.aux2[5];
+  if (I.op != GEVO_OP_BINARY || I.kin != GEVO_K_F64 || I.sub > GEVO_B_MAX || nops > 2)
+    return false;
+  const gevo_instr& X = (&I)[1];
+  int fsub[2] = {0, 0}, fleft[2] = {0, 0};
 #pragma unroll
   for (int m = 0; m < 2; ++m) {
-    f.fsub[m] = 0;
-    f.fleft[m] = 1;
-    f.e[m] = S.base[X->in[0].buf] + X->in[0].off;
-    f.s0[m] = f.s1[m] = 0;
-    if (m >= nops) continue;
-    const int w0 = X->aux[3 * m], w1 = X->aux[3 * m + 1];
+    if (m >= nops) break;
+    const int w0 = X.aux[3 * m], w1 = X.aux[3 * m + 1];
     const int cls = w0 & 15, sub = (w0 >> 4) & 15, kin = (w0 >> 8) & 15;
-    const int a = w1 & 255, b = (w1 >> 8) & 255;
+    const int s0 = w1 & 255, s1 = (w1 >> 8) & 255;
     const int prev = m == 0 ? 0 : GEVO_EPI_SRC_OP + m - 1;
     if (cls != GEVO_OP_BINARY || kin != GEVO_K_F64 || sub > GEVO_B_MAX) return false;
-    if (a == prev && b == m + 1) f.fleft[m] = 1;
-    else if (b == prev && a == m + 1) f.fleft[m] = 0;
+    if (s0 == prev && s1 == m + 1) fleft[m] = 1;
+    else if (s1 == prev && s0 == m + 1) fleft[m] = 0;
     else return false;
-    f.fsub[m] = sub;
-    // EXT operands are (r, c) views (lowering._as2d)
-    f.e[m] = S.base[X->in[m].buf] + X->in[m].off;
-    f.s0[m] = X->in[m].st[0];
-    f.s1[m] = X->in[m].st[1];
+    fsub[m] = sub;
   }
-  return true;
-}
-
-__device__ __forceinline__ double fast_chain_apply(const FastChain& f, double v, int r, int c) {
-#pragma unroll
-  for (int m = 0; m < 2; ++m) {
-    if (m >= f.nops) break;
-    const double x = f.e[m][r * f.s0[m] + c * f.s1[m]];
-    v = f.fleft[m] ? bin_f64(f.fsub[m], v, x) : bin_f64(f.fsub[m], x, v);
-  }
-  return v;
-}
-
-// fast form of an elementwise chain: an f64 binary op, then a FastChain.
-// Returns false for any other chain.
-__device__ __forceinline__ bool ew_chain_fast(const Shared& S, const gevo_instr& I) {
-  if (I.op != GEVO_OP_BINARY || I.kin != GEVO_K_F64 || I.sub > GEVO_B_MAX) return false;
-  FastChain f;
-  if (!fast_chain(S, &I + 1, I.aux2[5], f)) return false;
   const int n = I.n, rank = I.rank, sub = I.sub;
   const int C = rank == 2 ? I.shp[1] : (rank == 1 ? I.shp[0] : 1);
   auto st0 = [&](const gevo_operand& o) { return rank == 2 ? o.st[0] : 0; };
@@ -488,10 +510,19 @@ __device__ __forceinline__ bool ew_chain_fast(const Shared& S, const gevo_instr&
   const double* b = S.base[I.in[1].buf] + I.in[1].off;
   const int o0 = st0(I.out), o1 = st1(I.out), a0 = st0(I.in[0]), a1 = st1(I.in[0]);
   const int b0 = st0(I.in[1]), b1 = st1(I.in[1]);
+  // EXT operands are (r, c) views already (lowering._as2d)
+  const double* e0 = S.base[X.in[0].buf] + X.in[0].off;
+  const double* e1 = nops > 1 ? S.base[X.in[1].buf] + X.in[1].off : e0;
+  const int e00 = X.in[0].st[0], e01 = X.in[0].st[1];
+  const int e10 = nops > 1 ? X.in[1].st[0] : 0, e11 = nops > 1 ? X.in[1].st[1] : 0;
   for (int i = threadIdx.x; i < n; i += kThreads) {
     const int r = i / C, c = i - r * C;
-    const double v = bin_f64(sub, a[r * a0 + c * a1], b[r * b0 + c * b1]);
-    out[r * o0 + c * o1] = fast_chain_apply(f, v, r, c);
+    const double x0 = e0[r * e00 + c * e01];
+    const double x1 = nops > 1 ? e1[r * e10 + c * e11] : 0.0;
+    double v = bin_f64(sub, a[r * a0 + c * a1], b[r * b0 + c * b1]);
+    v = fleft[0] ? bin_f64(fsub[0], v, x0) : bin_f64(fsub[0], x0, v);
+    if (nops > 1) v = fleft[1] ? bin_f64(fsub[1], v, x1) : bin_f64(fsub[1], x1, v);
+    out[r * o0 + c * o1] = v;
   }
   return true;
 }
@@ -527,82 +558,6 @@ __device__ __noinline__ void run_ew_chain(Shared& S, const gevo_instr& I) {
     double ev[kEpiPre];
     epi_fetch(e, r, c, ev);
     p[0][r * s0[0] + c * s1[0]] = epilogue(e, ev, v, r, c);
-  }
-}
-
-// REDUCE (interpreter.py:138-142).  With a fused chain (aux2[0] EXT records,
-// aux2[1] micro-ops; lowering.fuse_ew_chains) the micro-ops are applied to
-// each reduced value before its store: the FastChain form in registers, any
-// other chain through the shared-memory decode.
-__device__ __noinline__ void run_reduce(Shared& S, const gevo_instr& I) {
-  const int n_ext = I.aux2[0];
-  FastChain fc;
-  fc.nops = 0;
-  bool generic = false;
-  if (n_ext > 0 && !fast_chain(S, &I + 1, I.aux2[1], fc)) {
-    if (threadIdx.x == 0) decode_epilogue(S, &I + 1, n_ext, I.aux2[1]);
-    __syncthreads();
-    generic = true;
-  }
-  double* out = opptr(S, I.out);
-  const double* in = opptr(S, I.in[0]);
-  // the record's fields into registers (stores may alias it)
-  const int L = I.aux[0], n = I.n, rank = I.rank, kin = I.kin, sub = I.sub;
-  const int64_t rs = I.aux[1];
-  int shp[GEVO_MAXR], ist[GEVO_MAXR], ost[GEVO_MAXR];
-#pragma unroll
-  for (int d = 0; d < GEVO_MAXR; ++d) {
-    shp[d] = I.shp[d];
-    ist[d] = I.in[0].st[d];
-    ost[d] = I.out.st[d];
-  }
-  const int ioff = I.in[0].off, ooff = I.out.off;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    int idx[GEVO_MAXR];
-    unravel(i, rank, shp, idx);
-    int src = ioff, dst = ooff;
-#pragma unroll
-    for (int d = 0; d < GEVO_MAXR; ++d) {
-      if (d < rank) {
-        src += idx[d] * ist[d];
-        dst += idx[d] * ost[d];
-      }
-    }
-    const double* p = in + src;
-    double r;
-    if (kin == GEVO_K_F64) {
-      if (sub == GEVO_R_MAX) {
-        r = p[0];
-        for (int k = 1; k < L; ++k) r = np_fmax(r, p[k * rs]);
-      } else if (sub == GEVO_R_SUM_PAIRWISE) {
-        r = pairwise_sum(p, L, rs);
-      } else {
-        r = 0.0;
-        for (int k = 0; k < L; ++k) r = __dadd_rn(r, p[k * rs]);
-      }
-    } else {
-      int64_t v;
-      if (sub == GEVO_R_MAX) {
-        v = as_i64(p[0]);
-        for (int k = 1; k < L; ++k) { int64_t x = as_i64(p[k * rs]); v = x > v ? x : v; }
-      } else {
-        uint64_t acc = 0;
-        for (int k = 0; k < L; ++k) acc += (uint64_t)as_i64(p[k * rs]);
-        v = (int64_t)acc;
-      }
-      r = as_w(v);
-    }
-    if (n_ext > 0) {
-      const int rr = rank == 2 ? idx[0] : 0, cc = rank == 2 ? idx[1] : (rank == 1 ? idx[0] : 0);
-      if (generic) {
-        double ev[kEpiPre];
-        epi_fetch(S.epi, rr, cc, ev);
-        r = epilogue(S.epi, ev, r, rr, cc);
-      } else {
-        r = fast_chain_apply(fc, r, rr, cc);
-      }
-    }
-    out[dst] = r;
   }
 }
 
@@ -690,7 +645,7 @@ __device__ __noinline__ void run_instrs(Shared& S, const gevo_instr* ins, int n,
           run_elementwise(S, I);
         }
         break;
-      case GEVO_OP_REDUCE: run_reduce(S, I); k += I.aux2[0]; break;
+      case GEVO_OP_REDUCE: run_reduce(S, I); break;
       case GEVO_OP_DOT: run_dot(S, I, stage); k += I.aux2[0]; break;
       case GEVO_OP_PAD: run_pad(S, I); break;
     }

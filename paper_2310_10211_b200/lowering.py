@@ -566,10 +566,7 @@ def fuse_ew_chains(instrs):
                     readers.setdefault(v.alloc, []).append((i, k, "ext"))
         touched, drop = set(), []
         for i, p in enumerate(instrs):
-            # producers: elementwise ops, and f64 reductions (the chain runs
-            # on each reduced value, e.g. b2' = b2 - lr * sum(g, 0))
-            if i in touched or not (p["op"] in _EW_OPS or
-                                    (p["op"] == OP_REDUCE and p["kin"] == K_F64)):
+            if p["op"] not in _EW_OPS or i in touched:
                 continue
             out = p["out"]
             if out.alloc < 0 or out.buf != BUF_ARENA or len(out.shape) > 2 or \

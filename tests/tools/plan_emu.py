@@ -115,8 +115,6 @@ def run(instrs, mem):
                     r = wd(np.max(x, axis=1) if sub == Lw.R_MAX else np.sum(x, axis=1))
                 else:
                     r = np.max(w, axis=1) if sub == Lw.R_MAX else np.sum(w, axis=1)
-                if rec.get("epi"):
-                    r = apply_epilogue(mem, rec, r)
             elif op == Lw.OP_DOT:
                 a, b = rec["in"]
                 M, N, K = shape[0], shape[1], rec["aux"][0]
