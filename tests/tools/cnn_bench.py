@@ -69,8 +69,60 @@ def profile(pop=128, n=100):
               f"{100 * cyc / tot:5.1f}%  count={cnt:9d}  cycles/instr={cyc / cnt:9.0f}")
 
 
+def full(pop=128, n=1000, batch=100, check=100):
+    """BASELINE.json configs[2] network: MobileNetV2-CIFAR width 0.5
+    (cnn.MOBILENETV2_CIFAR_HALF), batch 100, `n` images, the unmutated
+    forward replicated to `pop` (throughput of the full-size network), and a
+    parity check of its fitness against the oracle on the first `check`
+    images."""
+    cfg = cnn.CnnConfig(**cnn.MOBILENETV2_CIFAR_HALF, batch_size=batch, search_n=n,
+                        holdout_n=batch)
+    wl = cnn.build_cnn_prediction_workload(cfg)
+    fn = wl.module.functions["forward"]
+    macs = 0
+    types = dict(fn.params)
+    for op in fn.ops:
+        if op.opcode == "dot":
+            a, b = types[op.operands[0]], types[op.operands[1]]
+            macs += a.shape[0] * a.shape[1] * b.shape[1]
+        types[op.result] = op.result_type
+    ev = DeviceEvaluator(wl)
+    v = {"forward": fn}
+    t = time.perf_counter()
+    fits, rec = ev.evaluate_variants([v] * pop, return_records=True)
+    wall = time.perf_counter() - t
+    ms = ev.last_device_ms
+    flops = 2.0 * macs * (n // batch) * pop
+    print(f"full cnn (MobileNetV2-CIFAR 0.5, {macs / batch / 1e6:.1f} M dot MACs/img) pop {pop} x "
+          f"{n} images, batch {batch}: device {ms / 1e3:.2f} s -> {pop / ms * 1e3:.3f} ind/s "
+          f"({flops / ms / 1e9:.3f} TFLOP/s fp64 dot work), e2e {pop / wall:.3f} ind/s; "
+          f"{n * pop / (ms / 1e3):.0f} images/s; fitness {fits[0]}")
+    ev.close()
+    # parity on the first `check` images: device vs oracle
+    cfg2 = cnn.CnnConfig(**cnn.MOBILENETV2_CIFAR_HALF, batch_size=batch, search_n=check,
+                         holdout_n=batch)
+    wl2 = cnn.build_cnn_prediction_workload(cfg2)
+    ev2 = DeviceEvaluator(wl2)
+    (f_dev,), rec2 = ev2.evaluate_variants([{"forward": wl2.module.functions["forward"]}],
+                                           return_records=True)
+    ev2.close()
+    from oracle import fitness as OF
+    xs = wl2.search_x.reshape(-1, batch, 32, 32, 3)
+    t = time.perf_counter()
+    r = OF.evaluate_variant({"forward": wl2.module.functions["forward"]}, "prediction",
+                            [wl2.weights["w"]], (xs, wl2.search_y, wl2.search_labels))
+    dt = time.perf_counter() - t
+    print(f"parity on {check} images: device {f_dev.cost} {f_dev.error} (wrong {int(rec2['wrong'][0])}) "
+          f"oracle {r['cost']} {r['error']} (wrong {r['wrong']}) -> "
+          f"{'bit-exact' if (f_dev.cost, f_dev.error) == (r['cost'], r['error']) else 'DIFFERENT'}; "
+          f"oracle {dt:.1f} s for {check} images on 1 core "
+          f"({dt * 10000 / check / 60:.1f} min per 10k-image individual)")
+
+
 if __name__ == "__main__":
-    if sys.argv[1:2] == ["profile"]:
+    if sys.argv[1:2] == ["full"]:
+        full(*[int(a) for a in sys.argv[2:]])
+    elif sys.argv[1:2] == ["profile"]:
         profile(*[int(a) for a in sys.argv[2:]])
     else:
         main(*[int(a) for a in sys.argv[1:]])
