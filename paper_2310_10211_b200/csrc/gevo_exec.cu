@@ -527,7 +527,68 @@ __device__ __forceinline__ bool ew_chain_fast(const Shared& S, const gevo_instr&
   return true;
 }
 
+// rank 3..6 chains (always the fast form, lowering._fast_form): the output's
+// multi-index advances by kThreads in mixed radix (as ew_instr's N-d walk) and
+// every operand -- the op's two inputs and the EXT operands -- is addressed by
+// its own full strides.
+__device__ __noinline__ void ew_chain_nd(const Shared& S, const gevo_instr& I) {
+  const gevo_instr& X = (&I)[1];
+  const int nops = I.aux2[5], n = I.n, rank = I.rank, sub = I.sub;
+  int fsub[2] = {0, 0}, fleft[2] = {1, 1};
+  for (int m = 0; m < nops; ++m) {
+    const int w0 = X.aux[3 * m], w1 = X.aux[3 * m + 1];
+    fsub[m] = (w0 >> 4) & 15;
+    fleft[m] = (w1 & 255) == (m == 0 ? 0 : GEVO_EPI_SRC_OP + m - 1);
+  }
+  const gevo_operand* ops[5] = {&I.out, &I.in[0], &I.in[1], &X.in[0], &X.in[1]};
+  double* p[5];
+  int st[5][GEVO_MAXR], shp[GEVO_MAXR], idx[GEVO_MAXR], dig[GEVO_MAXR];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const bool used = k < 3 || k - 3 < nops;
+    p[k] = S.base[ops[k]->buf] + (used ? ops[k]->off : 0);
+#pragma unroll
+    for (int d = 0; d < GEVO_MAXR; ++d) st[k][d] = used ? ops[k]->st[d] : 0;
+  }
+#pragma unroll
+  for (int d = 0; d < GEVO_MAXR; ++d) shp[d] = I.shp[d];
+  unravel(threadIdx.x, rank, I.shp, idx);
+  unravel(kThreads, rank, I.shp, dig);
+  for (int base = threadIdx.x; base < n; base += kThreads) {
+    int ad[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      int v = 0;
+#pragma unroll
+      for (int d = 0; d < GEVO_MAXR; ++d)
+        if (d < rank) v += idx[d] * st[k][d];
+      ad[k] = v;
+    }
+    double v = bin_f64(sub, p[1][ad[1]], p[2][ad[2]]);
+    const double x0 = p[3][ad[3]];
+    v = fleft[0] ? bin_f64(fsub[0], v, x0) : bin_f64(fsub[0], x0, v);
+    if (nops > 1) {
+      const double x1 = p[4][ad[4]];
+      v = fleft[1] ? bin_f64(fsub[1], v, x1) : bin_f64(fsub[1], x1, v);
+    }
+    p[0][ad[0]] = v;
+    int carry = 0;
+#pragma unroll
+    for (int d = GEVO_MAXR - 1; d >= 0; --d) {
+      if (d < rank) {
+        const int w = idx[d] + dig[d] + carry;
+        carry = w >= shp[d];
+        idx[d] = carry ? w - shp[d] : w;
+      }
+    }
+  }
+}
+
 __device__ __noinline__ void run_ew_chain(Shared& S, const gevo_instr& I) {
+  if (I.rank > 2) {
+    ew_chain_nd(S, I);
+    return;
+  }
   if (ew_chain_fast(S, I)) return;
   if (threadIdx.x == 0) decode_epilogue(S, &I + 1, I.aux2[4], I.aux2[5]);
   __syncthreads();

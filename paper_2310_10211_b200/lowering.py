@@ -545,6 +545,24 @@ def _as2d(v: Val) -> Val:
     return Val(v.buf, v.off, (1, 1), (0, 0), v.kind, v.alloc)
 
 
+_B_MAX = B_CODES["maximum"]
+
+
+def _fast_form(p, epi) -> bool:
+    """An f64 add/sub/mul/div/max followed by <= 2 such micro-ops, micro-op m
+    combining the running value with epilogue operand m + 1 (the device's
+    FastChain)."""
+    if p["op"] != OP_BINARY or p["kin"] != K_F64 or p["sub"] > _B_MAX or len(epi) > 2:
+        return False
+    for m, (cls, sub, kin, _, srcs) in enumerate(epi):
+        prev = 0 if m == 0 else EPI_SRC_OP + m - 1
+        if cls != OP_BINARY or kin != K_F64 or sub > _B_MAX:
+            return False
+        if len(srcs) != 2 or sorted(srcs) != sorted([prev, m + 1]):
+            return False
+    return True
+
+
 def fuse_ew_chains(instrs):
     """Fold a single-use elementwise result into its elementwise consumer.
 
@@ -569,8 +587,8 @@ def fuse_ew_chains(instrs):
             if p["op"] not in _EW_OPS or i in touched:
                 continue
             out = p["out"]
-            if out.alloc < 0 or out.buf != BUF_ARENA or len(out.shape) > 2 or \
-                    math.prod(out.shape) > EW_CHAIN_MAX:
+            nd = len(out.shape) > 2
+            if out.alloc < 0 or out.buf != BUF_ARENA or math.prod(out.shape) > EW_CHAIN_MAX:
                 continue
             rs = readers.get(out.alloc, [])
             if len(rs) != 1 or rs[0][2] != "in":
@@ -594,7 +612,7 @@ def fuse_ew_chains(instrs):
                 if kk == k:
                     srcs.append(prev)
                 else:
-                    ext.append(_as2d(w))
+                    ext.append(w if nd else _as2d(w))
                     srcs.append(len(ext))    # 1-based operand index
             epi.append((r["op"], r["sub"], r["kin"], r["kout"], srcs))
             # R's own chain (from an earlier merge) follows, re-indexed: its
@@ -612,6 +630,10 @@ def fuse_ew_chains(instrs):
                         m.append(ext0 + x)
                 epi.append((cls, sub, kin, kout, m))
             ext.extend(r_ext)
+            # rank > 2 (CNN activations): only the fast form, addressed by the
+            # full multi-index on the device (run_ew_chain, N-d walk)
+            if nd and not _fast_form(p, epi):
+                continue
             new = dict(p)
             new["epi"], new["ext"], new["out"] = epi, ext, r["out"]
             instrs[j] = new

@@ -198,3 +198,40 @@ def test_returned_layout_cycles_are_exact():
         flags.append(vp.flags)
     assert not any(f & Lw.FLAG_LAYOUT_APPROX for f in flags)
     assert any(f & Lw.FLAG_ALTERNATE for f in flags)
+
+
+def _emulate_words(fn, args, fuse):
+    low = Lw.lower_function(fn, None, ret_layout="c", fuse=fuse)
+    consts = Lw.consts_to_words(low.consts).view(np.int64).copy() if low.consts \
+        else np.zeros(1, dtype=np.int64)
+    mem = {Lw.BUF_ARENA: np.zeros(max(low.arena_elems, 1), dtype=np.int64),
+           Lw.BUF_CONST: consts,
+           Lw.BUF_SMEM: np.zeros(max(low.smem_elems, 1), dtype=np.int64)}
+    for k, p in enumerate(args):
+        mem[Lw.BUF_PARAM0 + k] = _words(p)
+    for r, ty in enumerate(fn.return_types):
+        mem[Lw.BUF_OUT0 + r] = np.zeros(max(1, int(np.prod(ty.shape))), dtype=np.int64)
+    plan_emu.run(low.instrs, mem)
+    return [mem[Lw.BUF_OUT0 + r].copy() for r in range(len(fn.return_types))], low
+
+
+def test_fusion_changes_no_bit():
+    """Dot epilogues and elementwise chains (rank <= 2 and the CNN's rank-4
+    fast-form chains) emulate bit-identically to the unfused tables."""
+    from paper_2310_10211_b200 import cnn
+    cases = []
+    wl = W.build_2fcnet_workload()
+    args = [wl.weights[n] for n in W.WEIGHT_NAMES] + [wl.search_x[0], wl.search_y[0]]
+    for ind in load("train_pop.json.gz")["individuals"][:60]:
+        cases.append((dialect.parse_function(ind["train_step"]), args))
+    cw = cnn.build_cnn_prediction_workload(cnn.CnnConfig(search_n=20, holdout_n=10, batch_size=2))
+    cases.append((cw.module.functions["forward"],
+                  [cw.weights["w"], cw.search_x[0].reshape(2, 32, 32, 3)]))
+    nd = 0
+    for fn, a in cases:
+        fused, low = _emulate_words(fn, a, True)
+        plain, _ = _emulate_words(fn, a, False)
+        assert all(np.array_equal(x, y) for x, y in zip(fused, plain))
+        nd += sum(1 for r in low.instrs if r.get("epi") and r["op"] != Lw.OP_DOT
+                  and len(r["out"].shape) > 2)
+    assert nd > 0          # the CNN's depthwise taps fused
