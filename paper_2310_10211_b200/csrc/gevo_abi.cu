@@ -24,16 +24,20 @@ struct Split {
   int nb = 0, batch = 0, features = 0, classes = 0;
 };
 
+// Device buffer that grows on demand.  Growth is stream-ordered
+// (cudaFreeAsync / cudaMallocAsync on the owning context's stream): a plain
+// cudaFree synchronises the whole device, which serialised the two halves of
+// a generation running on two contexts whenever a buffer grew.
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
-  int ensure(size_t bytes) {
+  int ensure(size_t bytes, cudaStream_t st) {
     if (bytes <= cap) return 0;
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
     p = nullptr;
     cap = 0;
     size_t want = bytes + bytes / 4 + 256;
-    if (cudaMalloc(&p, want) != cudaSuccess) return -1;
+    if (cudaMallocAsync(&p, want, st) != cudaSuccess) return -1;
     cap = want;
     return 0;
   }
@@ -115,7 +119,7 @@ int parse_plan(gevo_ctx* ctx, const void* plan, size_t bytes, PlanView* v) {
 
 int upload_plan(gevo_ctx* ctx, const void* plan, size_t bytes, const PlanView& v,
                 const gevo_instr** di, const gevo_prog** dp, const double** dc) {
-  if (ctx->plan.ensure(bytes + 16)) return fail(ctx, GEVO_E_CUDA, "plan alloc failed");
+  if (ctx->plan.ensure(bytes + 16, ctx->stream)) return fail(ctx, GEVO_E_CUDA, "plan alloc failed");
   CK(cudaMemcpyAsync(ctx->plan.p, plan, bytes, cudaMemcpyHostToDevice, ctx->stream));
   char* base = static_cast<char*>(ctx->plan.p);
   *di = reinterpret_cast<const gevo_instr*>(base + v.instr_off);
@@ -366,12 +370,12 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   const double* dc;
   rc = upload_plan(ctx, plan, plan_bytes, v, &di, &dp, &dc);
   if (rc) return rc;
-  if (ctx->arena.ensure((size_t)h->total_elems * sizeof(double) + 64))
+  if (ctx->arena.ensure((size_t)h->total_elems * sizeof(double) + 64, ctx->stream))
     return fail(ctx, GEVO_E_CUDA, "arena alloc failed");
-  if (ctx->results.ensure((size_t)h->n_prog * sizeof(gevo_result)))
+  if (ctx->results.ensure((size_t)h->n_prog * sizeof(gevo_result), ctx->stream))
     return fail(ctx, GEVO_E_CUDA, "results alloc failed");
   if (final_weights &&
-      ctx->finalw.ensure((size_t)h->n_prog * h->weight_elems * sizeof(double) + 8))
+      ctx->finalw.ensure((size_t)h->n_prog * h->weight_elems * sizeof(double) + 8, ctx->stream))
     return fail(ctx, GEVO_E_CUDA, "final weight alloc failed");
 
   EvalArgs a;
@@ -410,7 +414,7 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   a.smem_elems = h->max_smem;
   a.prof = nullptr;
   if (ctx->profile) {
-    if (ctx->prof.ensure(GEVO_PROFILE_SLOTS * 2 * 8)) return fail(ctx, GEVO_E_CUDA, "profile alloc");
+    if (ctx->prof.ensure(GEVO_PROFILE_SLOTS * 2 * 8, ctx->stream)) return fail(ctx, GEVO_E_CUDA, "profile alloc");
     CK(cudaMemsetAsync(ctx->prof.p, 0, GEVO_PROFILE_SLOTS * 2 * 8, ctx->stream));
     a.prof = static_cast<unsigned long long*>(ctx->prof.p);
   }
@@ -477,8 +481,8 @@ int gevo_exec_once(gevo_ctx* ctx, const void* plan, size_t plan_bytes, const dou
   const double* dc;
   rc = upload_plan(ctx, plan, plan_bytes, v, &di, &dp, &dc);
   if (rc) return rc;
-  if (ctx->arena.ensure((size_t)h->total_elems * sizeof(double) + 64) ||
-      ctx->params.ensure(param_words * 8 + 8) || ctx->outs.ensure(out_words * 8 + 8))
+  if (ctx->arena.ensure((size_t)h->total_elems * sizeof(double) + 64, ctx->stream) ||
+      ctx->params.ensure(param_words * 8 + 8, ctx->stream) || ctx->outs.ensure(out_words * 8 + 8, ctx->stream))
     return fail(ctx, GEVO_E_CUDA, "exec-once alloc failed");
   CK(cudaMemcpyAsync(ctx->params.p, params, param_words * 8, cudaMemcpyHostToDevice,
                      ctx->stream));
@@ -513,7 +517,7 @@ static int nsga2_common(gevo_ctx* ctx, const double* cost, const double* error, 
   // layout: c[n] e[n] crowd[n] | rank order fstart(n+1) nf count ord0 ord1 fop chosen
   size_t dbl = 3 * (size_t)n * 8;
   size_t ints = (size_t)(8 * n + 2 + (keep > 0 ? keep : 0)) * 4;
-  if (ctx->ns.ensure(dbl + ints + 64)) return fail(ctx, GEVO_E_CUDA, "nsga2 alloc failed");
+  if (ctx->ns.ensure(dbl + ints + 64, ctx->stream)) return fail(ctx, GEVO_E_CUDA, "nsga2 alloc failed");
   double* d = static_cast<double*>(ctx->ns.p);
   int32_t* iv = reinterpret_cast<int32_t*>(d + 3 * (size_t)n);
   NsArgs a;
@@ -560,7 +564,7 @@ int gevo_archive_merge(gevo_ctx* ctx, const double* cost, const double* error, i
   *n_keep = 0;
   if (n == 0) return GEVO_OK;
   CK(cudaSetDevice(ctx->device));
-  if (ctx->ns.ensure(2 * (size_t)n * 8 + ((size_t)n + 2) * 4 + 64))
+  if (ctx->ns.ensure(2 * (size_t)n * 8 + ((size_t)n + 2) * 4 + 64, ctx->stream))
     return fail(ctx, GEVO_E_CUDA, "archive alloc failed");
   double* d = static_cast<double*>(ctx->ns.p);
   int32_t* iv = reinterpret_cast<int32_t*>(d + 2 * (size_t)n);
@@ -591,7 +595,7 @@ int gevo_hypervolume(gevo_ctx* ctx, const double* cost, const double* error, int
   *out = 0.0;
   if (n == 0) return GEVO_OK;
   CK(cudaSetDevice(ctx->device));
-  if (ctx->ns.ensure((5 * (size_t)n + 1) * 8 + (size_t)n * 4 + 64))
+  if (ctx->ns.ensure((5 * (size_t)n + 1) * 8 + (size_t)n * 4 + 64, ctx->stream))
     return fail(ctx, GEVO_E_CUDA, "hypervolume alloc failed");
   double* d = static_cast<double*>(ctx->ns.p);
   HvArgs a;

@@ -542,43 +542,65 @@ __device__ __noinline__ void ew_chain_nd(const Shared& S, const gevo_instr& I) {
   }
   const gevo_operand* ops[5] = {&I.out, &I.in[0], &I.in[1], &X.in[0], &X.in[1]};
   double* p[5];
-  int st[5][GEVO_MAXR], shp[GEVO_MAXR], idx[GEVO_MAXR], dig[GEVO_MAXR];
+  // the 5 operands' strides live in shared memory (broadcast reads): in
+  // registers they spill
+  __shared__ int st[5][GEVO_MAXR];
+  int shp[GEVO_MAXR], idx[GEVO_MAXR], dig[GEVO_MAXR];
+  if (threadIdx.x < 5 * GEVO_MAXR) {
+    const int k = threadIdx.x / GEVO_MAXR, d = threadIdx.x % GEVO_MAXR;
+    st[k][d] = (k < 3 || k - 3 < nops) && d < rank ? ops[k]->st[d] : 0;
+  }
 #pragma unroll
   for (int k = 0; k < 5; ++k) {
     const bool used = k < 3 || k - 3 < nops;
     p[k] = S.base[ops[k]->buf] + (used ? ops[k]->off : 0);
-#pragma unroll
-    for (int d = 0; d < GEVO_MAXR; ++d) st[k][d] = used ? ops[k]->st[d] : 0;
   }
 #pragma unroll
   for (int d = 0; d < GEVO_MAXR; ++d) shp[d] = I.shp[d];
+  __syncthreads();
   unravel(threadIdx.x, rank, I.shp, idx);
   unravel(kThreads, rank, I.shp, dig);
-  for (int base = threadIdx.x; base < n; base += kThreads) {
-    int ad[5];
+  // U elements per thread in flight: all loads first, then the math and
+  // the stores (memory-level parallelism, as ew_instr)
+  constexpr int U = 2;
+  for (int base = threadIdx.x; base < n; base += U * kThreads) {
+    int ao[U];
+    double a[U], b[U], x0[U], x1[U];
 #pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      int v = 0;
+    for (int u = 0; u < U; ++u) {
+      if (base + u * kThreads < n) {
+        int ad[5];
 #pragma unroll
-      for (int d = 0; d < GEVO_MAXR; ++d)
-        if (d < rank) v += idx[d] * st[k][d];
-      ad[k] = v;
+        for (int k = 0; k < 5; ++k) {
+          int v = 0;
+#pragma unroll
+          for (int d = 0; d < GEVO_MAXR; ++d)
+            if (d < rank) v += idx[d] * st[k][d];
+          ad[k] = v;
+        }
+        ao[u] = ad[0];
+        a[u] = p[1][ad[1]];
+        b[u] = p[2][ad[2]];
+        x0[u] = p[3][ad[3]];
+        x1[u] = nops > 1 ? p[4][ad[4]] : 0.0;
+      }
+      int carry = 0;
+#pragma unroll
+      for (int d = GEVO_MAXR - 1; d >= 0; --d) {
+        if (d < rank) {
+          const int w = idx[d] + dig[d] + carry;
+          carry = w >= shp[d];
+          idx[d] = carry ? w - shp[d] : w;
+        }
+      }
     }
-    double v = bin_f64(sub, p[1][ad[1]], p[2][ad[2]]);
-    const double x0 = p[3][ad[3]];
-    v = fleft[0] ? bin_f64(fsub[0], v, x0) : bin_f64(fsub[0], x0, v);
-    if (nops > 1) {
-      const double x1 = p[4][ad[4]];
-      v = fleft[1] ? bin_f64(fsub[1], v, x1) : bin_f64(fsub[1], x1, v);
-    }
-    p[0][ad[0]] = v;
-    int carry = 0;
 #pragma unroll
-    for (int d = GEVO_MAXR - 1; d >= 0; --d) {
-      if (d < rank) {
-        const int w = idx[d] + dig[d] + carry;
-        carry = w >= shp[d];
-        idx[d] = carry ? w - shp[d] : w;
+    for (int u = 0; u < U; ++u) {
+      if (base + u * kThreads < n) {
+        double v = bin_f64(sub, a[u], b[u]);
+        v = fleft[0] ? bin_f64(fsub[0], v, x0[u]) : bin_f64(fsub[0], x0[u], v);
+        if (nops > 1) v = fleft[1] ? bin_f64(fsub[1], v, x1[u]) : bin_f64(fsub[1], x1[u], v);
+        p[0][ao[u]] = v;
       }
     }
   }
