@@ -213,7 +213,8 @@ class DeviceEvaluator:
         # two halves when the pool is used: half A runs on the device (ctypes
         # releases the GIL) while half B is still being lowered
         halves = [idx]
-        if len(idx) >= 2 * POOL_MIN and _lower_pool() is not None:
+        if len(idx) >= 2 * POOL_MIN and _lower_pool() is not None and \
+                os.environ.get("GEVO_B200_HALVES", "1") != "0":
             halves = [idx[:len(idx) // 2], idx[len(idx) // 2:]]
         jobs = [_submit_lowering(variants, h, cfg.cost_table, training, cfg.steps) for h in halves]
         ctxs = [self.ctx, self._second_context() if len(halves) > 1 else None]
@@ -263,15 +264,16 @@ class DeviceEvaluator:
         for key in used:
             (res, fw), lowered, slots, order = box[key]
             self._learn_layout(res, order)
+            records[np.asarray(slots, dtype=np.int64)] = res
+            status, wrong, total = (res["status"].tolist(), res["wrong"].tolist(),
+                                    res["total"].tolist())
             for k, vp in enumerate(lowered):
                 i = slots[k]
-                r = res[k]
-                records[i] = r
                 cost = vp.train_cost * cfg.steps if training else vp.fwd_cost * n_score
-                if r["status"] != STATUS_OK:
+                if status[k] != STATUS_OK:
                     fits[i] = Fitness(cost, 1.0)
                 else:
-                    fits[i] = Fitness(cost, int(r["wrong"]) / int(r["total"]))
+                    fits[i] = Fitness(cost, wrong[k] / total[k])
                 if want_weights:
                     finals[i] = fw[k]
         self.last_plan_bytes = plan_bytes

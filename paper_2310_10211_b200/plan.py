@@ -31,6 +31,8 @@ class VariantPlan:
     flags: int
     train_cost: float
     fwd_cost: float
+    w_train: float = 0.0          # fn_weight(train1) / fn_weight(fwd), computed where
+    w_fwd: float = 0.0            # the variant is lowered (a pool worker), not in the parent
 
 
 def _count(shape):
@@ -97,7 +99,7 @@ def lower_variant(functions: dict, cost_table=None, training=True,
     arena = max(arena, lowf.arena_elems)
     smem = max(smem, lowf.smem_elems)
     return VariantPlan(t0, t1, f, consts_to_words(consts), arena, smem, flags,
-                       train_cost, lowf.cost)
+                       train_cost, lowf.cost, fn_weight(t1), fn_weight(f))
 
 
 def _encode_shifted(low, pool):
@@ -121,26 +123,36 @@ OP_DOT = 5
 _MODE_WEIGHT = {0: 1.0, 1: 2.0, 3: 2.0, 2: 3.0}
 
 
+def fn_weight(arr) -> float:
+    """Estimated device time of one invocation of an encoded function: dot
+    MACs weighted by the kernel path their summation order takes, plus
+    element counts of the other instructions."""
+    if arr is None or len(arr) == 0:
+        return 0.0
+    op = arr["op"].astype(np.int64)
+    shp = arr["shp"].astype(np.float64)
+    aux = arr["aux"].astype(np.int64)
+    dot = op == OP_DOT
+    w = 0.0
+    if dot.any():
+        m, n, k = shp[dot, 0], shp[dot, 1], aux[dot, 0].astype(np.float64)
+        split = np.minimum(aux[dot, 1].astype(np.float64), n)
+        w1 = _MODE_LUT[np.clip(arr["sub"][dot].astype(np.int64), 0, 4)]
+        w2 = _MODE_LUT[np.clip(aux[dot, 2], 0, 4)]
+        w += float(np.sum(m * k * (split * w1 + (n - split) * w2) + 20000.0))
+    other = ~dot & (op != 7)
+    if other.any():
+        w += float(np.sum(4.0 * arr["n"][other].astype(np.float64) + 4000.0))
+    return w
+
+
+_MODE_LUT = np.array([_MODE_WEIGHT.get(i, 3.0) for i in range(5)])
+
+
 def device_weight(v: VariantPlan, steps: int = 600, batches: int = 31) -> float:
-    """Estimated device time of one individual: dot MACs weighted by the
-    kernel path their summation order takes, plus element counts of the other
-    instructions, over the train and scoring invocations."""
-    def fn_weight(arr):
-        if arr is None:
-            return 0.0
-        w = 0.0
-        for r in arr:
-            op = int(r["op"])
-            if op == OP_DOT:
-                m, n, k = int(r["shp"][0]), int(r["shp"][1]), int(r["aux"][0])
-                split = min(int(r["aux"][1]), n)
-                w += m * k * (split * _MODE_WEIGHT.get(int(r["sub"]), 3.0)
-                              + (n - split) * _MODE_WEIGHT.get(int(r["aux"][2]), 3.0))
-                w += 20000.0
-            elif op != 7:
-                w += 4.0 * int(r["n"]) + 4000.0
-        return w
-    return steps * fn_weight(v.train1) + batches * fn_weight(v.fwd)
+    """Estimated device time of one individual over its train and scoring
+    invocations (per-function weights from lowering time)."""
+    return steps * v.w_train + batches * v.w_fwd
 
 
 def sm_aware_order(weights, n_sms: int):
