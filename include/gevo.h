@@ -133,6 +133,10 @@ int gevo_download_split(gevo_ctx* ctx, int split_id, double* x, double* y,
  * C order, in @train_step return order */
 int gevo_upload_weights(gevo_ctx* ctx, const double* w, int64_t n_elems);
 
+/* One launch over the plan's programs.  results[prog.result_slot] receives
+ * each individual's record (the caller sizes `results` for header.n_prog
+ * records); programs that share a slot are the score parts of one
+ * prediction-mode individual (GEVO_FLAG_PART) and are merged here. */
 int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
               const gevo_eval_desc* desc, gevo_result* results,
               double* final_weights);

@@ -100,6 +100,14 @@ typedef struct {
 /* gevo_prog.flags */
 #define GEVO_FLAG_LAYOUT_APPROX 1     /* returned layouts had no period <= 2 */
 #define GEVO_FLAG_ALTERNATE 2         /* steps >= 1: odd -> train1, even -> train0 */
+/* Score parts (prediction mode only): an individual's scored batches are
+ * independent (fitness.py:361-368), so n_parts programs may share one
+ * result_slot, part j scoring batches j, j + n_parts, ...  gevo_eval merges
+ * them into results[result_slot] with integer sums (bit-exact). */
+#define GEVO_FLAG_PART_SHIFT 8        /* bits 8..19: this program's part */
+#define GEVO_FLAG_NPARTS_SHIFT 20     /* bits 20..30: parts of its individual (0 = 1) */
+#define GEVO_FLAG_PART(f) (((f) >> GEVO_FLAG_PART_SHIFT) & 0xFFF)
+#define GEVO_FLAG_NPARTS(f) ((((f) >> GEVO_FLAG_NPARTS_SHIFT) & 0x7FF) ? (((f) >> GEVO_FLAG_NPARTS_SHIFT) & 0x7FF) : 1)
 
 typedef struct {
   int32_t train0, train0_n;           /* @train_step, step 0 */

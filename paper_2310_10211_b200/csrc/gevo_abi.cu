@@ -113,6 +113,10 @@ int parse_plan(gevo_ctx* ctx, const void* plan, size_t bytes, PlanView* v) {
       return fail(ctx, GEVO_E_ARG, "prog instruction range out of bounds");
     if (p.arena_off < 0 || p.arena_off > h->total_elems)
       return fail(ctx, GEVO_E_ARG, "prog arena offset out of bounds");
+    if (p.result_slot < 0 || p.result_slot >= h->n_prog)
+      return fail(ctx, GEVO_E_ARG, "prog result slot out of bounds");
+    if (GEVO_FLAG_PART(p.flags) >= GEVO_FLAG_NPARTS(p.flags))
+      return fail(ctx, GEVO_E_ARG, "prog score part out of range");
   }
   return 0;
 }
@@ -126,6 +130,32 @@ int upload_plan(gevo_ctx* ctx, const void* plan, size_t bytes, const PlanView& v
   *dp = reinterpret_cast<const gevo_prog*>(base + v.prog_off);
   *dc = reinterpret_cast<const double*>(base + v.const_off);
   return 0;
+}
+
+// per-program records -> results[result_slot]: a whole individual is copied;
+// score parts add their integer counts, a non-finite part makes the whole
+// individual non-finite (the reference stops at its first non-finite batch
+// and returns error 1.0 whichever batch it was), timings span the parts
+void merge_results(const gevo_prog* progs, int n_prog, const gevo_result* per_prog, gevo_result* out) {
+  std::vector<uint8_t> done((size_t)n_prog, 0);
+  for (int i = 0; i < n_prog; ++i) {
+    const int s = progs[i].result_slot;
+    const gevo_result& r = per_prog[i];
+    gevo_result& o = out[s];
+    if (!done[s]) { o = r; done[s] = 1; continue; }
+    if (o.status == GEVO_STATUS_OK && r.status == GEVO_STATUS_OK) {
+      o.wrong += r.wrong;
+      o.total += r.total;
+    } else if (o.status == GEVO_STATUS_OK) {
+      o.status = r.status;
+      o.wrong = o.total = 0;
+    }
+    o.steps_run = r.steps_run > o.steps_run ? r.steps_run : o.steps_run;
+    o.cycles = r.cycles > o.cycles ? r.cycles : o.cycles;
+    o.t0_ns = r.t0_ns < o.t0_ns ? r.t0_ns : o.t0_ns;
+    o.t1_ns = r.t1_ns > o.t1_ns ? r.t1_ns : o.t1_ns;
+    if (GEVO_FLAG_PART(progs[i].flags) == 0) o.smid = r.smid;
+  }
 }
 
 }  // namespace
@@ -365,6 +395,34 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   if (h->n_weights < 0 || h->n_weights > GEVO_MAXP - 2)
     return fail(ctx, GEVO_E_ARG, "bad weight count");
 
+  // score parts: every result slot needs each of its n_parts programs once;
+  // training programs are never split (their steps are sequential)
+  const gevo_prog* hp = reinterpret_cast<const gevo_prog*>(static_cast<const char*>(plan) + v.prog_off);
+  {
+    std::vector<int32_t> nparts(h->n_prog, 0);
+    std::vector<uint8_t> seen;
+    bool split = false;
+    for (int i = 0; i < h->n_prog; ++i) split |= GEVO_FLAG_NPARTS(hp[i].flags) > 1;
+    if (split && desc->mode == GEVO_MODE_TRAIN)
+      return fail(ctx, GEVO_E_ARG, "score parts in a training plan");
+    for (int i = 0; i < h->n_prog; ++i) {
+      const int slot = hp[i].result_slot, np = GEVO_FLAG_NPARTS(hp[i].flags);
+      if (nparts[slot] == 0) nparts[slot] = np;
+      else if (nparts[slot] != np) return fail(ctx, GEVO_E_ARG, "inconsistent score parts");
+    }
+    std::vector<int64_t> first(h->n_prog, 0);
+    int64_t cells = 0;
+    for (int s = 0; s < h->n_prog; ++s) { first[s] = cells; cells += nparts[s]; }
+    seen.assign((size_t)cells, 0);
+    for (int i = 0; i < h->n_prog; ++i) {
+      uint8_t& c = seen[(size_t)(first[hp[i].result_slot] + GEVO_FLAG_PART(hp[i].flags))];
+      if (c) return fail(ctx, GEVO_E_ARG, "duplicate result slot / score part");
+      c = 1;
+    }
+    for (int64_t c = 0; c < cells; ++c)
+      if (!seen[(size_t)c]) return fail(ctx, GEVO_E_ARG, "result slot missing a score part");
+  }
+
   const gevo_instr* di;
   const gevo_prog* dp;
   const double* dc;
@@ -424,13 +482,15 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   launch_eval(a, h->n_prog, ctx->stream);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
-  CK(cudaMemcpyAsync(results, ctx->results.p, (size_t)h->n_prog * sizeof(gevo_result),
+  std::vector<gevo_result> per_prog((size_t)h->n_prog);
+  CK(cudaMemcpyAsync(per_prog.data(), ctx->results.p, (size_t)h->n_prog * sizeof(gevo_result),
                      cudaMemcpyDeviceToHost, ctx->stream));
   if (final_weights)
     CK(cudaMemcpyAsync(final_weights, ctx->finalw.p,
                        (size_t)h->n_prog * h->weight_elems * sizeof(double),
                        cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  merge_results(hp, h->n_prog, per_prog.data(), results);
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   ctx->last_ms = ms;

@@ -840,7 +840,10 @@ eval_kernel(EvalArgs args) {
   if (status == GEVO_STATUS_OK) {
     const gevo_instr* fw = stage(cache, args.instrs + P.fwd, P.fwd_n);
     const int B = args.batch, C = args.classes;
-    for (int b = 0; b < args.score_nb; ++b) {
+    // score parts (prediction mode): this program scores every n_parts-th batch
+    const int part = args.mode == GEVO_MODE_TRAIN ? 0 : GEVO_FLAG_PART(P.flags);
+    const int parts = args.mode == GEVO_MODE_TRAIN ? 1 : GEVO_FLAG_NPARTS(P.flags);
+    for (int b = part; b < args.score_nb; b += parts) {
       if (threadIdx.x == 0) {
         S.base[GEVO_BUF_ARENA] = scratch;
         S.base[GEVO_BUF_SMEM] = smem_arena;
@@ -869,7 +872,7 @@ eval_kernel(EvalArgs args) {
     }
   }
   if (threadIdx.x == 0) {
-    gevo_result* R = args.results + P.result_slot;
+    gevo_result* R = args.results + blockIdx.x;   // per program; gevo_eval merges by result_slot
     R->wrong = status == GEVO_STATUS_OK ? wrong : 0;
     R->total = status == GEVO_STATUS_OK ? total : 0;
     R->status = status;

@@ -235,10 +235,14 @@ class DeviceEvaluator:
             if not lowered:
                 continue
             wts = [device_weight(v, cfg.steps if training else 0, n_score) for v in lowered]
-            layout = self._sm_layout.get(len(lowered))
-            order = layout_order(wts, layout) if layout else sm_aware_order(wts, self.n_sms)
+            parts = 1 if training else self.score_parts(lowered, n_score, len(idx))
+            if parts > 1:
+                order = np.argsort(-np.asarray(wts), kind="stable")
+            else:
+                layout = self._sm_layout.get(len(lowered))
+                order = layout_order(wts, layout) if layout else sm_aware_order(wts, self.n_sms)
             plan = build_population_plan(lowered, self.weight_shapes, self.batch * self.classes,
-                                         order=order)
+                                         order=order, parts=parts)
             tc = time.perf_counter()
             t_lower += tb - ta
             t_pack += tc - tb
@@ -246,7 +250,7 @@ class DeviceEvaluator:
             args = (plan.blob, plan.n_prog, 0 if training else 1, cfg.steps if training else 0,
                     cfg.finite_check_every, SPLIT_SEARCH, split, self.weight_elems, want_weights)
 
-            def run(c=ctxs[h], a=args, key=h, lv=lowered, sl=slots, od=order):
+            def run(c=ctxs[h], a=args, key=h, lv=lowered, sl=slots, od=order if parts == 1 else None):
                 box[key] = (c.eval(*a), lv, sl, od)
             if h + 1 < len(jobs):
                 import threading
@@ -263,7 +267,9 @@ class DeviceEvaluator:
             self.last_device_ms = ctxs[used[0]].last_kernel_ms()
         for key in used:
             (res, fw), lowered, slots, order = box[key]
-            self._learn_layout(res, order)
+            res = res[:len(lowered)]          # records by result slot (score parts merged)
+            if order is not None:
+                self._learn_layout(res, order)
             records[np.asarray(slots, dtype=np.int64)] = res
             status, wrong, total = (res["status"].tolist(), res["wrong"].tolist(),
                                     res["total"].tolist())
@@ -286,6 +292,26 @@ class DeviceEvaluator:
         if want_weights:
             out.append(finals)
         return out[0] if len(out) == 1 else tuple(out)
+
+    def score_parts(self, lowered, n_score, n_total=None):
+        """Programs per prediction-mode individual (plan.build_population_plan
+        `parts`): enough to give the launch two CTAs per SM, at most one per
+        scored batch, and within GEVO_B200_ARENA_GB (default 64) of scratch.
+        `n_total` is the call's individual count when this launch holds one
+        half of it (the halves run concurrently).  GEVO_B200_PARTS overrides."""
+        n = len(lowered)
+        if n == 0 or n_score <= 1:
+            return 1
+        env = os.environ.get("GEVO_B200_PARTS")
+        if env:
+            return max(1, min(int(env), n_score))
+        parts = max(1, min(n_score, (2 * self.n_sms) // max(n, n_total or 0)))
+        per = sum(8 * ((v.arena + 15) & ~15) for v in lowered) + \
+            8 * n * (self.batch * self.classes + 2 * self.weight_elems + 48)
+        budget = float(os.environ.get("GEVO_B200_ARENA_GB", "64")) * 1e9
+        while parts > 1 and parts * per > budget:
+            parts -= 1
+        return parts
 
     def split_weights(self, flat):
         out, o = {}, 0

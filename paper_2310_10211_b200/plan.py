@@ -216,58 +216,84 @@ class PopulationPlan:
     total_elems: int
 
 
+FLAG_PART_SHIFT = 8        # gevo_plan.h GEVO_FLAG_PART / GEVO_FLAG_NPARTS
+FLAG_NPARTS_SHIFT = 20
+MAX_PARTS = 0x7FF
+
+
 def build_population_plan(variants: list[VariantPlan], weight_shapes,
-                          probs_elems: int, order=None) -> PopulationPlan:
+                          probs_elems: int, order=None, parts: int = 1) -> PopulationPlan:
     """Pack variants into one blob.  `order` is the launch order (CTA i runs
     individual order[i]); by default longest static cost first, so the
-    slowest individuals start in the first wave."""
+    slowest individuals start in the first wave.
+
+    parts > 1 (prediction mode only): each individual becomes `parts`
+    programs sharing its result slot, part j scoring batches j, j + parts,
+    ... on its own CTA and scratch (gevo_eval merges the records).  CTAs go
+    part-major, so the first wave holds part 0 of every individual."""
     n = len(variants)
     if order is None:
         key = np.array([v.train_cost * 1.0 + v.fwd_cost for v in variants])
         order = np.argsort(-key, kind="stable")
+    parts = int(parts)
+    if not 1 <= parts <= MAX_PARTS:
+        raise ValueError(f"score parts {parts} outside 1..{MAX_PARTS}")
+    if parts > 1 and any(v.train0 is not None for v in variants):
+        raise ValueError("score parts apply to prediction plans only")
+    if parts > 1:
+        order = [int(i) for j in range(parts) for i in order]
     wsizes = [_count(s) for s in weight_shapes]
     wofs = np.concatenate([[0], np.cumsum(wsizes)]).astype(np.int64)
     wtotal = int(wofs[-1])
     instr_chunks, const_chunks = [], []
-    progs = np.zeros(n, dtype=PROG_DTYPE)
+    progs = np.zeros(len(order), dtype=PROG_DTYPE)
     n_instr = n_const = 0
     elem = 0
     max_arena = 0
     max_smem = 0
+    placed = {}                             # individual -> its program row (code shared by parts)
     for slot, idx in enumerate(order):
         v = variants[idx]
+        if idx in placed:
+            progs[slot] = progs[placed[idx]]
         p = progs[slot]
-        p["result_slot"] = idx
-        p["const_off"] = n_const
-        const_chunks.append(v.consts)
-        n_const += len(v.consts)
-        if v.train0 is not None:
-            a = v.train0
-            p["train0"], p["train0_n"] = n_instr, len(a)
-            instr_chunks.append(a)
-            n_instr += len(a)
-            if v.train1 is v.train0:
-                p["train1"], p["train1_n"] = p["train0"], p["train0_n"]
-            else:
-                b = v.train1
-                p["train1"], p["train1_n"] = n_instr, len(b)
-                instr_chunks.append(b)
-                n_instr += len(b)
-        f = v.fwd
-        p["fwd"], p["fwd_n"] = n_instr, len(f)
-        instr_chunks.append(f)
-        n_instr += len(f)
+        if idx in placed:
+            p["result_slot"] = idx
+        else:
+            placed[idx] = slot
+            p["result_slot"] = idx
+            p["const_off"] = n_const
+            const_chunks.append(v.consts)
+            n_const += len(v.consts)
+            if v.train0 is not None:
+                a = v.train0
+                p["train0"], p["train0_n"] = n_instr, len(a)
+                instr_chunks.append(a)
+                n_instr += len(a)
+                if v.train1 is v.train0:
+                    p["train1"], p["train1_n"] = p["train0"], p["train0_n"]
+                else:
+                    b = v.train1
+                    p["train1"], p["train1_n"] = n_instr, len(b)
+                    instr_chunks.append(b)
+                    n_instr += len(b)
+            f = v.fwd
+            p["fwd"], p["fwd_n"] = n_instr, len(f)
+            instr_chunks.append(f)
+            n_instr += len(f)
         arena = (v.arena + 15) & ~15
         p["arena_off"] = elem
         p["arena_elems"] = arena
         p["flags"] = v.flags
+        if parts > 1:
+            p["flags"] = v.flags | ((slot // n) << FLAG_PART_SHIFT) | (parts << FLAG_NPARTS_SHIFT)
         max_arena = max(max_arena, arena)
         max_smem = max(max_smem, v.smem)
         # [scratch | probs | weights ping | weights pong], 16-element aligned
         elem += arena + ((probs_elems + 15) & ~15) + 2 * ((wtotal + 15) & ~15)
     hdr = np.zeros(1, dtype=HEADER_DTYPE)
     hdr["magic"], hdr["version"] = PLAN_MAGIC, PLAN_VERSION
-    hdr["n_instr"], hdr["n_prog"], hdr["n_const"] = n_instr, n, n_const
+    hdr["n_instr"], hdr["n_prog"], hdr["n_const"] = n_instr, len(order), n_const
     hdr["weight_elems"] = wtotal
     hdr["n_weights"] = len(wsizes)
     hdr["wofs"][0, :len(wsizes)] = wofs[:-1]
@@ -279,7 +305,7 @@ def build_population_plan(variants: list[VariantPlan], weight_shapes,
     consts = np.concatenate(const_chunks) if const_chunks else np.zeros(0)
     blob = np.concatenate([hdr.view(np.uint8), instrs.view(np.uint8),
                            progs.view(np.uint8), consts.view(np.uint8)])
-    return PopulationPlan(blob, n, np.asarray(order), elem)
+    return PopulationPlan(blob, len(order), np.asarray(order), elem)
 
 
 def exec_once_plan(fns, param_arrays_list):

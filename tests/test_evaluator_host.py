@@ -106,3 +106,96 @@ def test_sm_aware_order_places_heaviest_alone_and_pairs_heavy_with_light():
     assert max(sums) - min(sums) <= 1.0               # heavy paired with light
     # outside one wave: heaviest first
     assert sm_aware_order(w[:100], n_sms).tolist() == list(range(99, -1, -1))
+
+
+def _merge_records(progs, per_prog, n):
+    """Python restatement of gevo_abi.cu merge_results (score parts)."""
+    out = np.zeros(n, dtype=_lib.RESULT_DTYPE)
+    done = set()
+    for p, r in zip(progs, per_prog):
+        s = int(p["result_slot"])
+        if s not in done:
+            out[s] = r
+            done.add(s)
+        elif out[s]["status"] == E.STATUS_OK and r["status"] == E.STATUS_OK:
+            out[s]["wrong"] += r["wrong"]
+            out[s]["total"] += r["total"]
+        elif out[s]["status"] == E.STATUS_OK:
+            out[s]["status"], out[s]["wrong"], out[s]["total"] = r["status"], 0, 0
+    return out
+
+
+class PartsContext(FakeContext):
+    """Emulates one prediction launch: each program scores the batches its
+    score part owns (GEVO_FLAG_PART / NPARTS); batch b counts b + 1 wrong,
+    and the launch's individual 3 sees non-finite probabilities on batch 5
+    only; the records are merged as gevo_eval merges them."""
+    n_batches = 31
+
+    def eval(self, blob, n_prog, mode, steps, check_every, train_split, score_split,
+             weight_elems=0, want_weights=False):
+        from paper_2310_10211_b200.lowering import INSTR_DTYPE, PROG_DTYPE
+        from paper_2310_10211_b200.plan import FLAG_NPARTS_SHIFT, FLAG_PART_SHIFT
+        hdr = blob[:HEADER_DTYPE.itemsize].view(HEADER_DTYPE)[0]
+        o = HEADER_DTYPE.itemsize + int(hdr["n_instr"]) * INSTR_DTYPE.itemsize
+        progs = blob[o:o + n_prog * PROG_DTYPE.itemsize].view(PROG_DTYPE)
+        self.plans.append(n_prog)
+        per = np.zeros(n_prog, dtype=_lib.RESULT_DTYPE)
+        arenas = set()
+        for k, p in enumerate(progs):
+            part = (int(p["flags"]) >> FLAG_PART_SHIFT) & 0xFFF
+            parts = ((int(p["flags"]) >> FLAG_NPARTS_SHIFT) & 0x7FF) or 1
+            i = int(p["result_slot"])
+            arenas.add(int(p["arena_off"]))
+            for b in range(part, self.n_batches, parts):
+                if i == 3 and b == 5:
+                    per[k]["status"], per[k]["wrong"], per[k]["total"] = E.STATUS_NONFINITE_PROBS, 0, 0
+                    break
+                per[k]["wrong"] += b + 1
+                per[k]["total"] += 32
+        assert len(arenas) == n_prog                   # every program has its own scratch
+        n = len({int(p["result_slot"]) for p in progs})
+        self.parts = n_prog // n
+        return _merge_records(progs, per, n_prog), None
+
+
+_PW = []
+
+
+def _predict_workload():
+    """predict2fc with the unfrozen initial weights (no training pass: the
+    weights' values do not matter to the plan layout under test)."""
+    if not _PW:
+        wl = W.build_2fcnet_workload()
+        wl.mode = W.PREDICTION
+        _PW.append(wl)
+    return _PW[0]
+
+
+@pytest.mark.parametrize("n,forced", [(7, None), (40, None), (7, "3"), (150, None)])
+def test_prediction_score_parts_cover_every_batch_once(monkeypatch, n, forced):
+    wl = _predict_workload()
+    FakeContext.instances = []
+    monkeypatch.setattr(_lib, "Context", PartsContext)
+    monkeypatch.setattr(_lib, "span_ms", lambda a, b: 2.0)
+    if forced:
+        monkeypatch.setenv("GEVO_B200_PARTS", forced)
+    nb = len(wl.dataset.search.labels) // wl.config.batch_size
+    PartsContext.n_batches = nb
+    fns = [{"forward": wl.module.functions["forward"]}] * n
+    ev = E.DeviceEvaluator(wl)
+    fits, recs = ev.evaluate_variants(fns, return_records=True)
+    ctx = ev.ctx
+    expect_parts = int(forced) if forced else max(1, min(nb, 2 * 148 // n))
+    assert ctx.parts == expect_parts
+    bad = 0
+    for f, r in zip(fits, recs):
+        if r["status"] != E.STATUS_OK:
+            assert r["status"] == E.STATUS_NONFINITE_PROBS and f.error == 1.0
+            bad += 1
+            continue
+        assert r["total"] == 32 * nb
+        assert r["wrong"] == nb * (nb + 1) // 2       # every batch exactly once
+        assert f.error == r["wrong"] / r["total"]
+    assert bad == sum(len(c.plans) for c in FakeContext.instances)  # slot 3 of each launch
+    ev.close()

@@ -195,6 +195,27 @@ def test_predict_population_fitness():
     assert exact >= 0.95 * len(inds)
 
 
+def test_prediction_score_parts_identical_records(monkeypatch):
+    """Score parts (several CTAs per prediction individual, each scoring every
+    n-th batch, merged in gevo_eval) give the records of one CTA per
+    individual, bit for bit; both match the reference's fitness."""
+    inds = load("predict_pop.json.gz")["individuals"][:24]
+    wl = W.build_prediction_workload(weights=predict_weights())
+    fns = [variant_functions(i, ("forward",)) for i in inds]
+    out = {}
+    for parts in ("1", "7", "31"):
+        monkeypatch.setenv("GEVO_B200_PARTS", parts)
+        ev = DeviceEvaluator(wl)
+        fits, rec = ev.evaluate_variants(fns, return_records=True)
+        ev.close()
+        out[parts] = (fits, [rec[k].tolist() for k in ("wrong", "total", "status")])
+    for parts in ("7", "31"):
+        assert out[parts][0] == out["1"][0]
+        assert out[parts][1] == out["1"][1]
+    exact = sum(f.error == i["error"] and f.cost == i["cost"] for f, i in zip(out["7"][0], inds))
+    print(f"score parts 1/7/31 identical; bit-exact vs reference {exact}/{len(inds)}")
+
+
 def test_holdout_reports(train_wl):
     hold = load("train_pop.json.gz")["holdout"]
     ev = DeviceEvaluator(train_wl)
