@@ -1156,8 +1156,8 @@ __device__ __noinline__ void dot_panels_pipe(const DotArgs& dref, int col0, int 
 
 // CK: 0 FMA_CHAIN, 1 ACC8 (8 lane chains (k mod 8) per output, each on its
 // own DMMA accumulator tile, chain j's four k of a chunk (j, j+8, j+16, j+24)
-// read from the unpermuted tile with stride 8; warp = one 8x8 tile, <= 16
-// columns), 2 SEQ_NOFMA, 3 integer (scalar; thread = 4 outputs of the panel).
+// read from the unpermuted tile with stride 8; warp = an 8x16 strip, two
+// tiles x 8 chains, so a 32-column piece is one pass), 2 SEQ_NOFMA, 3 integer (scalar; thread = 4 outputs of the panel).
 template <bool PANELS, int CK>
 __device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, double* stage_buf,
                                       const EpiDev* epi, int mode) {
@@ -1220,10 +1220,10 @@ __device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, d
     if (i < total) load(i, i);
     cp_async_commit();
   }
-  const int rb = warp >> 1, cb0 = ACC8 ? (warp & 1) : (warp & 1) * 2;
+  const int rb = warp >> 1, cb0 = (warp & 1) * 2;      // warp = 8 x 16 strip (two tiles)
   const int lm = rb * 8 + g, ln = cb0 * 8 + 2 * t4;
   const int kmain = (ACC8 && mode == GEVO_D_ACC8_TAIL) ? (K & ~7) : K;
-  constexpr int NACC = ACC8 ? 16 : 4;
+  constexpr int NACC = ACC8 ? 32 : 4;                  // ACC8: 2 tiles x 8 chains x 2
   double acc[NACC];
 #pragma unroll
   for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
@@ -1244,7 +1244,7 @@ __device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, d
     const int pm = PANELS ? min(kPanel, M - s * kPanel) : M;
     const int nk = PANELS ? K : min(kKC, K - s * kKC);    const bool last = PANELS || s == total - 1;
     const bool act0 = !SCALAR && rb * 8 < pm && cb0 * 8 < ncols;
-    const bool act1 = !ACC8 && act0 && (cb0 + 1) * 8 < ncols;
+    const bool act1 = act0 && (cb0 + 1) * 8 < ncols;
     if (SCALAR) {
       // the thread's 4 outputs (rows mm + 8u, column nn) advance together so
       // their 4 dependent chains overlap; invalid rows compute garbage that is
@@ -1274,10 +1274,13 @@ __device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, d
       const int k0 = PANELS ? 0 : s * kKC;
       const double* pa = As + lm * ars + 8 * t4 * aks;
       const double* pb = Bs + (cb0 * 8 + g) * brs + 8 * t4 * bks;
+      const double* pb1 = pb + 8 * brs;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         if (k0 + j + 24 < kmain) {
-          dmma884(acc[2 * j], acc[2 * j + 1], pa[j * aks], pb[j * bks]);
+          const double a = pa[j * aks];
+          dmma884(acc[2 * j], acc[2 * j + 1], a, pb[j * bks]);
+          if (act1) dmma884(acc[16 + 2 * j], acc[17 + 2 * j], a, pb1[j * bks]);
         } else {
 #pragma unroll 1
           for (int t = 0; t < 4; ++t) {
@@ -1286,6 +1289,10 @@ __device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, d
             const double a = As[lm * ars + kk * aks];
             acc[2 * j] = fma(a, Bs[ln * brs + kk * bks], acc[2 * j]);
             acc[2 * j + 1] = fma(a, Bs[(ln + 1) * brs + kk * bks], acc[2 * j + 1]);
+            if (act1) {
+              acc[16 + 2 * j] = fma(a, Bs[(ln + 8) * brs + kk * bks], acc[16 + 2 * j]);
+              acc[17 + 2 * j] = fma(a, Bs[(ln + 9) * brs + kk * bks], acc[17 + 2 * j]);
+            }
           }
         }
       }
@@ -1294,16 +1301,24 @@ __device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, d
         const bool avx = (PANELS ? s * kPanel : 0) + lm >= d.xrow;
         double r0 = lane_tree(acc, 0, avx);
         double r1 = lane_tree(acc, 1, avx);
+        double r2 = lane_tree(acc + 16, 0, avx);
+        double r3 = lane_tree(acc + 16, 1, avx);
 #pragma unroll 1
         for (int kk = kmain - k0; kk < nk; ++kk) {
           const double a = As[lm * ars + kk * aks];
           r0 = fma(a, Bs[ln * brs + kk * bks], r0);
           r1 = fma(a, Bs[(ln + 1) * brs + kk * bks], r1);
+          if (act1) {
+            r2 = fma(a, Bs[(ln + 8) * brs + kk * bks], r2);
+            r3 = fma(a, Bs[(ln + 9) * brs + kk * bks], r3);
+          }
         }
 #pragma unroll
         for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
         acc[0] = r0;
         acc[1] = r1;
+        acc[2] = r2;
+        acc[3] = r3;
       }
     } else if (!ACC8 && act0) {
       const double* pa = As + lm * ars + t4 * aks;
@@ -1358,7 +1373,7 @@ __device__ __noinline__ void dot_fast(const DotArgs& dref, int col0, int col1, d
       } else if (act0) {
         Cs[lm * kCS + ln] = acc[0];
         Cs[lm * kCS + ln + 1] = acc[1];
-        if (!ACC8) {
+        if (!ACC8 || act1) {
           Cs[lm * kCS + ln + 8] = acc[2];
           Cs[lm * kCS + ln + 9] = acc[3];
         }
@@ -1530,10 +1545,10 @@ __device__ __forceinline__ void dot_columns(const DotArgs& d, int col0, int col1
                                             double* stage_buf, const EpiDev* epi) {
   if (col0 >= col1) return;
   // fast paths (one <= 32-row panel with K streamed, or K <= 32 with rows
-  // streamed), in column pieces of <= 32 (<= 16 for ACC8); the general
+  // streamed), in column pieces of <= 32; the general
   // pipeline otherwise
   const int ck = integer ? 3 : (mode == GEVO_D_SEQ_NOFMA ? 2 : (mode == GEVO_D_FMA_CHAIN ? 0 : 1));
-  const int width = ck == 1 ? 16 : kPanel;
+  const int width = kPanel;
   if (ck <= 1 && d.M <= kPanel && d.K <= kKC && col1 - col0 <= (ck == 1 ? 16 : kPanel)) {
     dot_tiny_dispatch(d, col0, col1, epi, ck == 1, mode);
     return;
