@@ -119,7 +119,39 @@ def full(pop=128, n=1000, batch=100, check=100):
           f"({dt * 10000 / check / 60:.1f} min per 10k-image individual)")
 
 
+def fullprof(pop=128, n=200, batch=100):
+    """per-instruction-class cycles of the full-size network (configs[2])"""
+    cfg = cnn.CnnConfig(**cnn.MOBILENETV2_CIFAR_HALF, batch_size=batch, search_n=n,
+                        holdout_n=batch)
+    wl = cnn.build_cnn_prediction_workload(cfg)
+    v = {"forward": wl.module.functions["forward"]}
+    ev = DeviceEvaluator(wl)
+    ev.evaluate_variants([v] * 4)
+    ev.ctx.profile(True)
+    ev.evaluate_variants([v] * pop)
+    prof = ev.ctx.profile(False)
+    tot = sum(c for c, _ in prof.values())
+    print(f"full cnn profile: pop {pop} x {n} images, kernel {ev.last_device_ms:.1f} ms")
+    OPS = {1: "unary", 2: "binary", 3: "select", 4: "reduce", 5: "dot", 6: "pad"}
+    for (op, sub, big), (cyc, cnt) in sorted(prof.items(), key=lambda kv: -kv[1][0])[:16]:
+        print(f"{OPS.get(op, op):7s} sub={sub:2d} {'big' if big else 'small':5s} "
+              f"{100 * cyc / tot:5.1f}%  count={cnt:9d}  cycles/instr={cyc / cnt:9.0f}")
+    # the dots of the network: shape, summation order, operand strides
+    from paper_2310_10211_b200.plan import lower_variant
+    vp = lower_variant(v, None, training=False, steps=0)
+    for r in vp.fwd:
+        if r["op"] == 5:
+            print("  DOT M,N,K", int(r["shp"][0]), int(r["shp"][1]), int(r["aux"][0]),
+                  "mode", int(r["sub"]), int(r["aux"][2]),
+                  "A st", tuple(int(x) for x in r["in"][0]["st"][:2]),
+                  "B st", tuple(int(x) for x in r["in"][1]["st"][:2]))
+    ev.close()
+
+
 if __name__ == "__main__":
+    if sys.argv[1:2] == ["fullprof"]:
+        fullprof(*[int(a) for a in sys.argv[2:]])
+        sys.exit(0)
     if sys.argv[1:2] == ["full"]:
         full(*[int(a) for a in sys.argv[2:]])
     elif sys.argv[1:2] == ["profile"]:
