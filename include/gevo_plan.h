@@ -50,8 +50,13 @@ enum {
   GEVO_OP_DOT = 5,     /* sub: GEVO_D_* for columns < aux[1]; aux[2] for the
                           rest; aux[0]=K */
   GEVO_OP_PAD = 6,     /* aux[d]=low[d], aux2[d]=input extent[d] */
-  GEVO_OP_EXT = 7      /* continuation record of the preceding DOT: a fused
+  GEVO_OP_EXT = 7,     /* continuation record of the preceding DOT: a fused
                           elementwise epilogue (see below) */
+  GEVO_OP_TAPSUM = 8   /* f64 sum of products: v = in0*in1, then v = v + x_t*y_t
+                          for taps t = 1 .. aux2[5]-1, each product and sum
+                          rounded on its own; (x_t, y_t) are the operands of
+                          the aux2[4] EXT records that follow, 3 per record.
+                          All x share in[0]'s strides, all y in[1]'s. */
 };
 
 /* Dot epilogues.  A DOT whose aux2[0] = E > 0 is followed by E GEVO_OP_EXT

@@ -680,6 +680,81 @@ __device__ __noinline__ void run_dot(Shared& S, const gevo_instr& I, double* sta
   dot_columns(d, split, N, I.aux[2], integer, stage, epi);
 }
 
+// GEVO_OP_TAPSUM (lowering.fuse_tap_sums; the CNN's depthwise 3x3): per
+// output element, v = x0*y0, then v = v + xt*yt for each further tap, with
+// the multiply and add roundings of the instructions it replaces.  The taps
+// share their x strides and their y strides, so one N-d walk gives every
+// tap's offset; the tap base pointers are read from shared memory.
+constexpr int kTapMax = 9;
+__device__ __noinline__ void run_tapsum(Shared& S, const gevo_instr& I) {
+  const int ntap = I.aux2[5], n = I.n, rank = I.rank;
+  __shared__ const double* tx[kTapMax];
+  __shared__ const double* ty[kTapMax];
+  __shared__ int sx[GEVO_MAXR], sy[GEVO_MAXR], so[GEVO_MAXR];
+  if (threadIdx.x < ntap) {
+    const int t = threadIdx.x;
+    const int ex = 2 * (t - 1), ey = ex + 1;      // operand index among the EXT records
+    const gevo_operand& X = t == 0 ? I.in[0] : (&I)[1 + ex / 3].in[ex % 3];
+    const gevo_operand& Y = t == 0 ? I.in[1] : (&I)[1 + ey / 3].in[ey % 3];
+    tx[t] = S.base[X.buf] + X.off;
+    ty[t] = S.base[Y.buf] + Y.off;
+  }
+  if (threadIdx.x < GEVO_MAXR) {
+    const int d = threadIdx.x;
+    sx[d] = d < rank ? I.in[0].st[d] : 0;
+    sy[d] = d < rank ? I.in[1].st[d] : 0;
+    so[d] = d < rank ? I.out.st[d] : 0;
+  }
+  double* out = S.base[I.out.buf] + I.out.off;
+  int idx[GEVO_MAXR], dig[GEVO_MAXR], shp[GEVO_MAXR];
+#pragma unroll
+  for (int d = 0; d < GEVO_MAXR; ++d) shp[d] = I.shp[d];
+  unravel(threadIdx.x, rank, I.shp, idx);
+  unravel(kThreads, rank, I.shp, dig);
+  __syncthreads();
+  constexpr int U = 2;
+  for (int base = threadIdx.x; base < n; base += U * kThreads) {
+    int ax[U], ay[U], ao[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int a = 0, b = 0, c = 0;
+#pragma unroll
+      for (int d = 0; d < GEVO_MAXR; ++d)
+        if (d < rank) {
+          a += idx[d] * sx[d];
+          b += idx[d] * sy[d];
+          c += idx[d] * so[d];
+        }
+      ax[u] = a;
+      ay[u] = b;
+      ao[u] = c;
+      int carry = 0;
+#pragma unroll
+      for (int d = GEVO_MAXR - 1; d >= 0; --d) {
+        if (d < rank) {
+          const int w = idx[d] + dig[d] + carry;
+          carry = w >= shp[d];
+          idx[d] = carry ? w - shp[d] : w;
+        }
+      }
+    }
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      v[u] = base + u * kThreads < n ? __dmul_rn(tx[0][ax[u]], ty[0][ay[u]]) : 0.0;
+    for (int t = 1; t < ntap; ++t) {
+      const double* px = tx[t];
+      const double* py = ty[t];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (base + u * kThreads < n) v[u] = __dadd_rn(v[u], __dmul_rn(px[ax[u]], py[ay[u]]));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (base + u * kThreads < n) out[ao[u]] = v[u];
+  }
+}
+
 // profile slot of an instruction: op class x sub-op x size bucket
 __device__ __forceinline__ int prof_slot(const gevo_instr& I) {
   const int big = I.n >= 4096 ? 1 : 0;
@@ -729,6 +804,7 @@ __device__ __noinline__ void run_instrs(Shared& S, const gevo_instr* ins, int n,
         }
         break;
       case GEVO_OP_REDUCE: run_reduce(S, I); break;
+      case GEVO_OP_TAPSUM: run_tapsum(S, I); k += I.aux2[4]; break;
       case GEVO_OP_DOT: run_dot(S, I, stage); k += I.aux2[0]; break;
       case GEVO_OP_PAD: run_pad(S, I); break;
     }

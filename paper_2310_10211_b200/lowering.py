@@ -43,6 +43,8 @@ SMEM_BUDGET = 3968
 K_F64, K_I64, K_I1 = 0, 1, 2
 KIND = {"f32": K_F64, "i32": K_I64, "i1": K_I1}
 OP_UNARY, OP_BINARY, OP_SELECT, OP_REDUCE, OP_DOT, OP_PAD, OP_EXT = 1, 2, 3, 4, 5, 6, 7
+OP_TAPSUM = 8          # sum of products, one pass (fuse_tap_sums, gevo_plan.h)
+TAP_MAX = 9
 EPI_SRC_OP = 64
 EPI_MAX_OPS = 8        # micro-ops fused into one dot epilogue
 EPI_MAX_EXT = 6        # extra operands (3 per continuation record)
@@ -645,6 +647,78 @@ def fuse_ew_chains(instrs):
             del instrs[i]
 
 
+def fuse_tap_sums(instrs):
+    """Fold a running sum of products into one TAPSUM instruction.
+
+    The pattern is the CNN's depthwise 3x3 (cnn.py depthwise): p_i = x_i * y_i
+    (f64 multiply), s_1 = p_0 + p_1, s_i = s_(i-1) + p_i, every p_i and every
+    partial sum s_i read exactly once, through the identity view, by the next
+    add.  All x_i must share one stride vector, and so must all y_i (the taps
+    are windows of one padded tensor times broadcast per-channel weights).
+    The TAPSUM computes v = x_0*y_0, then v = v + x_i*y_i for i >= 1, each
+    product and each sum rounded on its own (__dmul_rn / __dadd_rn, like the
+    multiply and add instructions it replaces), so fusion changes no bit.
+    The partial sums and the products are never stored: per output element
+    the taps are read once and the sum written once, instead of a product
+    and a running-sum round trip per tap."""
+    readers = {}
+    for i, r in enumerate(instrs):
+        for k, v in enumerate(list(r["in"]) + list(r.get("ext", []))):
+            if v.alloc >= 0:
+                readers.setdefault(v.alloc, []).append((i, k))
+
+    def single_use_into(i, j):
+        """instrs[i]'s result is read once, by instrs[j], through its own view."""
+        o = instrs[i]["out"]
+        if o.alloc < 0 or o.buf != BUF_ARENA:
+            return False
+        rs = readers.get(o.alloc, [])
+        return len(rs) == 1 and rs[0][0] == j and _same_view(instrs[j]["in"][rs[0][1]], o)
+
+    def plain(r, sub):
+        return (r["op"] == OP_BINARY and r["sub"] == sub and r["kin"] == K_F64 and
+                not r.get("epi") and not r.get("ext") and len(r["out"].shape) >= 1)
+
+    producer = {}
+    for i, r in enumerate(instrs):
+        if r["out"].alloc >= 0:
+            producer[r["out"].alloc] = i
+    sums = {}           # index of a chain's last add -> (taps [(x, y)], members)
+    for j, r in enumerate(instrs):
+        if not plain(r, B_CODES["add"]):
+            continue
+        shape = tuple(r["out"].shape)
+        srcs = [producer.get(v.alloc, -1) if v.alloc >= 0 else -1 for v in r["in"]]
+        muls = [i for i in srcs if i >= 0 and plain(instrs[i], B_CODES["multiply"]) and
+                tuple(instrs[i]["out"].shape) == shape and single_use_into(i, j)]
+        prev = [i for i in srcs if i in sums and single_use_into(i, j)]
+        if prev and muls:
+            taps, members = sums[prev[0]]
+            m = [i for i in muls if i != prev[0]]
+            if not m or len(taps) >= TAP_MAX:
+                continue
+            del sums[prev[0]]
+            sums[j] = (taps + [m[0]], members + [prev[0], m[0]])
+        elif len(muls) == 2 and muls[0] != muls[1]:
+            a, b = (muls if srcs[0] == muls[0] else muls[::-1])
+            sums[j] = ([a, b], [a, b])
+    drop = set()
+    for j, (taps, members) in sums.items():
+        xs = [instrs[i]["in"][0] for i in taps]
+        ys = [instrs[i]["in"][1] for i in taps]
+        if len({tuple(v.st) for v in xs}) != 1 or len({tuple(v.st) for v in ys}) != 1:
+            continue
+        rec = dict(instrs[j])
+        rec["op"], rec["sub"] = OP_TAPSUM, len(taps)
+        rec["in"] = [xs[0], ys[0]]
+        rec["ext"] = [v for x, y in zip(xs[1:], ys[1:]) for v in (x, y)]
+        instrs[j] = rec
+        drop.update(members)
+    for i in sorted(drop, reverse=True):
+        del instrs[i]
+    return instrs
+
+
 def lower_function(fn, param_layouts=None, ret_bufs=None, ret_layout="compact",
                    cost_table=None, smem_budget=None, fuse=True) -> Lowered:
     """Lower one function.  Params i live in buffer PARAM0+i with the given
@@ -661,6 +735,7 @@ def lower_function(fn, param_layouts=None, ret_bufs=None, ret_layout="compact",
     ret_st = b.run(fn.returns)
     if fuse:
         fuse_dot_epilogues(b.instrs)
+        fuse_tap_sums(b.instrs)
         fuse_ew_chains(b.instrs)
     top, stop = b.assign_arena(smem_budget)
     # resolve arena offsets into the operands
@@ -731,7 +806,15 @@ def encode_instrs(instrs, const_base=0) -> np.ndarray:
     for rec in instrs:
         recs = [rec]
         n_ext = n_epi = 0
-        if rec.get("epi"):
+        if rec["op"] == OP_TAPSUM:
+            # taps 1.. as (x_i, y_i) operand pairs, 3 per continuation record
+            exts = _ext_records({"ext": rec["ext"]})
+            rec = dict(rec)
+            aux2 = [0] * MAXR
+            aux2[4], aux2[5] = len(exts), rec["sub"]
+            rec["aux2"] = aux2
+            recs = [rec] + exts
+        elif rec.get("epi"):
             exts = _ext_records(rec)
             n_ext, n_epi = len(exts), len(rec["epi"])
             rec = dict(rec)

@@ -234,4 +234,6 @@ def test_fusion_changes_no_bit():
         assert all(np.array_equal(x, y) for x, y in zip(fused, plain))
         nd += sum(1 for r in low.instrs if r.get("epi") and r["op"] != Lw.OP_DOT
                   and len(r["out"].shape) > 2)
-    assert nd > 0          # the CNN's depthwise taps fused
+    assert nd > 0          # the CNN's BN chains fused
+    taps = [r["sub"] for r in low.instrs if r["op"] == Lw.OP_TAPSUM]
+    assert taps and all(t == 9 for t in taps)          # every depthwise 3x3 is one TAPSUM

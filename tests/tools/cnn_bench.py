@@ -132,15 +132,15 @@ def fullprof(pop=128, n=200, batch=100):
     prof = ev.ctx.profile(False)
     tot = sum(c for c, _ in prof.values())
     print(f"full cnn profile: pop {pop} x {n} images, kernel {ev.last_device_ms:.1f} ms")
-    OPS = {1: "unary", 2: "binary", 3: "select", 4: "reduce", 5: "dot", 6: "pad"}
+    OPS = {0: "tapsum", 1: "unary", 2: "binary", 3: "select", 4: "reduce", 5: "dot", 6: "pad"}
     for (op, sub, big), (cyc, cnt) in sorted(prof.items(), key=lambda kv: -kv[1][0])[:16]:
-        print(f"{OPS.get(op, op):7s} sub={sub:2d} {'big' if big else 'small':5s} "
+        print(f"{OPS.get(op, str(op)):7s} sub={sub:2d} {'big' if big else 'small':5s} "
               f"{100 * cyc / tot:5.1f}%  count={cnt:9d}  cycles/instr={cyc / cnt:9.0f}")
     # the dots of the network: shape, summation order, operand strides
     from paper_2310_10211_b200.plan import lower_variant
     vp = lower_variant(v, None, training=False, steps=0)
     for r in vp.fwd:
-        if r["op"] == 5:
+        if r["op"] == 5 and False:
             print("  DOT M,N,K", int(r["shp"][0]), int(r["shp"][1]), int(r["aux"][0]),
                   "mode", int(r["sub"]), int(r["aux"][2]),
                   "A st", tuple(int(x) for x in r["in"][0]["st"][:2]),

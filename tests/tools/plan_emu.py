@@ -123,6 +123,13 @@ def run(instrs, mem):
                 r = (wd(fl(A) @ fl(B)) if kin == F else A @ B).reshape(-1)
                 if rec.get("epi"):
                     r = apply_epilogue(mem, rec, r)
+            elif op == Lw.OP_TAPSUM:
+                xs = [rec["in"][0]] + rec["ext"][0::2]
+                ys = [rec["in"][1]] + rec["ext"][1::2]
+                v = fl(gather(mem, xs[0], shape)) * fl(gather(mem, ys[0], shape))
+                for x, y in zip(xs[1:], ys[1:]):
+                    v = v + fl(gather(mem, x, shape)) * fl(gather(mem, y, shape))
+                r = wd(v)
             elif op == Lw.OP_PAD:
                 a, pv = rec["in"]
                 low, ext_ = rec["aux"][:len(shape)], rec["aux2"][:len(shape)]
