@@ -216,6 +216,50 @@ def test_prediction_score_parts_identical_records(monkeypatch):
     print(f"score parts 1/7/31 identical; bit-exact vs reference {exact}/{len(inds)}")
 
 
+def test_score_part_plans_are_validated():
+    """gevo_eval refuses plans whose score parts are inconsistent: a missing or
+    duplicated part, a part index out of range, or parts in a training
+    launch (no kernel runs; GevoError carries the reason)."""
+    from paper_2310_10211_b200 import _lib
+    from paper_2310_10211_b200.evaluator import lower_all
+    from paper_2310_10211_b200.lowering import HEADER_DTYPE, INSTR_DTYPE, PROG_DTYPE
+    from paper_2310_10211_b200.plan import FLAG_NPARTS_SHIFT, FLAG_PART_SHIFT, build_population_plan
+    inds = load("predict_pop.json.gz")["individuals"][:3]
+    wl = W.build_prediction_workload(weights=predict_weights())
+    ev = DeviceEvaluator(wl)
+    vps = lower_all([variant_functions(i, ("forward",)) for i in inds], None, False, 0)
+    plan = build_population_plan(vps, ev.weight_shapes, ev.batch * ev.classes, parts=2)
+    hdr = plan.blob[:HEADER_DTYPE.itemsize].view(HEADER_DTYPE)[0]
+    o = HEADER_DTYPE.itemsize + int(hdr["n_instr"]) * INSTR_DTYPE.itemsize
+
+    def run(blob, mode=1):
+        return ev.ctx.eval(blob, plan.n_prog, mode, 0 if mode else 600, 50, 0, 0, ev.weight_elems, False)
+    res, _ = run(plan.blob)                                   # the valid plan runs
+    assert ((res["total"][:3] == 32 * 31) | (res["status"][:3] != 0)).all()
+
+    def corrupt(fn):
+        blob = plan.blob.copy()
+        progs = blob[o:o + plan.n_prog * PROG_DTYPE.itemsize].view(PROG_DTYPE)
+        fn(progs)
+        return blob
+    cases = {
+        "duplicate": lambda p: p.__setitem__("flags", np.where(
+            np.arange(len(p)) == 3, p["flags"] & ~(0xFFF << FLAG_PART_SHIFT), p["flags"])),
+        "part out of range": lambda p: p.__setitem__("flags", p["flags"] | (5 << FLAG_PART_SHIFT)),
+        "inconsistent": lambda p: p.__setitem__("flags", np.where(
+            np.arange(len(p)) == 0, (p["flags"] & ~(0x7FF << FLAG_NPARTS_SHIFT)) | (3 << FLAG_NPARTS_SHIFT),
+            p["flags"])),
+        "slot out of range": lambda p: p.__setitem__("result_slot", np.where(
+            np.arange(len(p)) == 1, 99, p["result_slot"])),
+    }
+    for name, fn in cases.items():
+        with pytest.raises(_lib.GevoError):
+            run(corrupt(fn))
+    with pytest.raises(_lib.GevoError):
+        run(plan.blob, mode=0)                                 # parts in a training launch
+    ev.close()
+
+
 def test_holdout_reports(train_wl):
     hold = load("train_pop.json.gz")["holdout"]
     ev = DeviceEvaluator(train_wl)
