@@ -531,6 +531,76 @@ __device__ __forceinline__ bool ew_chain_fast(const Shared& S, const gevo_instr&
 // multi-index advances by kThreads in mixed radix (as ew_instr's N-d walk) and
 // every operand -- the op's two inputs and the EXT operands -- is addressed by
 // its own full strides.
+//
+// Channel form: when every operand is C-ordered, a scalar, or a last-dim
+// (per-channel) broadcast -- the CNN's folded batch norm, x * scale[c] +
+// bias[c] then max(., 0) -- element i is at i, at 0, or at i mod C, and the
+// walk is a running channel index instead of the N-d digits.
+__device__ __forceinline__ int chan_kind(const gevo_operand& o, const gevo_instr& I) {
+  int cst = 1;
+  bool lin = true, scal = true, chan = true;
+  for (int d = I.rank - 1; d >= 0; --d) {
+    const int e = I.shp[d], st = o.st[d];
+    if (e != 1) {
+      lin &= st == cst;
+      scal &= st == 0;
+      chan &= d == I.rank - 1 ? st == 1 : st == 0;
+    }
+    cst *= e;
+  }
+  return lin ? 0 : (scal ? 1 : (chan ? 2 : -1));
+}
+
+__device__ __noinline__ bool ew_chain_chan(const Shared& S, const gevo_instr& I, const int* fsub,
+                                           const int* fleft) {
+  const gevo_instr& X = (&I)[1];
+  const int nops = I.aux2[5], n = I.n, sub = I.sub, C = I.shp[I.rank - 1];
+  const gevo_operand* ops[5] = {&I.out, &I.in[0], &I.in[1], &X.in[0], &X.in[1]};
+  int kind[5];
+  const double* p[5];
+  for (int k = 0; k < 5; ++k) {
+    const bool used = k < 3 || k - 3 < nops;
+    kind[k] = used ? chan_kind(*ops[k], I) : 1;
+    if (kind[k] < 0 || (k == 0 && kind[k] != 0)) return false;
+    p[k] = S.base[ops[k]->buf] + (used ? ops[k]->off : 0);
+  }
+  double* out = S.base[I.out.buf] + I.out.off;
+  constexpr int U = 2;
+  int c0 = threadIdx.x % C;
+  const int c1 = kThreads % C, cstep = (U * kThreads) % C;
+  for (int base = threadIdx.x; base < n; base += U * kThreads) {
+    double a[U], b[U], x0[U], x1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * kThreads;
+      int c = c0 + u * c1;
+      if (c >= C) c -= C;
+      int ad[5];
+#pragma unroll
+      for (int k = 1; k < 5; ++k) ad[k] = kind[k] == 0 ? i : (kind[k] == 2 ? c : 0);
+      if (i < n) {
+        a[u] = p[1][ad[1]];
+        b[u] = p[2][ad[2]];
+        x0[u] = p[3][ad[3]];
+        x1[u] = nops > 1 ? p[4][ad[4]] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * kThreads;
+      if (i < n) {
+        double v = bin_f64(sub, a[u], b[u]);
+        v = fleft[0] ? bin_f64(fsub[0], v, x0[u]) : bin_f64(fsub[0], x0[u], v);
+        if (nops > 1) v = fleft[1] ? bin_f64(fsub[1], v, x1[u]) : bin_f64(fsub[1], x1[u], v);
+        out[i] = v;
+      }
+    }
+    c0 += cstep;
+    if (c0 >= C) c0 -= C;
+  }
+  return true;
+}
+
 __device__ __noinline__ void ew_chain_nd(const Shared& S, const gevo_instr& I) {
   const gevo_instr& X = (&I)[1];
   const int nops = I.aux2[5], n = I.n, rank = I.rank, sub = I.sub;
@@ -540,6 +610,7 @@ __device__ __noinline__ void ew_chain_nd(const Shared& S, const gevo_instr& I) {
     fsub[m] = (w0 >> 4) & 15;
     fleft[m] = (w1 & 255) == (m == 0 ? 0 : GEVO_EPI_SRC_OP + m - 1);
   }
+  if (ew_chain_chan(S, I, fsub, fleft)) return;
   const gevo_operand* ops[5] = {&I.out, &I.in[0], &I.in[1], &X.in[0], &X.in[1]};
   double* p[5];
   // the 5 operands' strides live in shared memory (broadcast reads): in
