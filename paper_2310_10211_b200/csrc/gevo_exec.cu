@@ -267,28 +267,40 @@ __device__ __noinline__ void run_pad(const Shared& S, const gevo_instr& I) {
     is[d] = I.in[0].st[d];
     os[d] = I.out.st[d];
   }
-  for (int i = threadIdx.x; i < n; i += kThreads) {
-    bool inside = true;
-    int src = ioff, dst = ooff;
+  // U elements per thread in flight: the loads of all U first, then the stores
+  constexpr int U = 4;
+  for (int base = threadIdx.x; base < n; base += U * kThreads) {
+    int dsts[U];
+    double v[U];
 #pragma unroll
-    for (int d = 0; d < GEVO_MAXR; ++d) {
-      if (d < rank) {
-        const int j = idx[d] - lo[d];
-        inside = inside && j >= 0 && j < ex[d];
-        src += j * is[d];
-        dst += idx[d] * os[d];
+    for (int u = 0; u < U; ++u) {
+      bool inside = true;
+      int src = ioff, dst = ooff;
+#pragma unroll
+      for (int d = 0; d < GEVO_MAXR; ++d) {
+        if (d < rank) {
+          const int j = idx[d] - lo[d];
+          inside = inside && j >= 0 && j < ex[d];
+          src += j * is[d];
+          dst += idx[d] * os[d];
+        }
+      }
+      dsts[u] = dst;
+      v[u] = pv;
+      if (inside && base + u * kThreads < n) v[u] = in[src];
+      int carry = 0;
+#pragma unroll
+      for (int d = GEVO_MAXR - 1; d >= 0; --d) {
+        if (d < rank) {
+          const int w = idx[d] + dig[d] + carry;
+          carry = w >= shp[d];
+          idx[d] = carry ? w - shp[d] : w;
+        }
       }
     }
-    out[dst] = inside ? in[src] : pv;
-    int carry = 0;
 #pragma unroll
-    for (int d = GEVO_MAXR - 1; d >= 0; --d) {
-      if (d < rank) {
-        int v = idx[d] + dig[d] + carry;
-        carry = v >= shp[d];
-        idx[d] = carry ? v - shp[d] : v;
-      }
-    }
+    for (int u = 0; u < U; ++u)
+      if (base + u * kThreads < n) out[dsts[u]] = v[u];
   }
 }
 
