@@ -56,7 +56,10 @@ enum {
                           for taps t = 1 .. aux2[5]-1, each product and sum
                           rounded on its own; (x_t, y_t) are the operands of
                           the aux2[4] EXT records that follow, 3 per record.
-                          All x share in[0]'s strides, all y in[1]'s. */
+                          All x share in[0]'s strides, all y in[1]'s.
+                          aux2[3] = M <= 3 epilogue micro-ops applied before
+                          the store: aux[m] = GEVO_B_* | left << 4, operand m
+                          = EXT operand 2*(taps-1) + m (its own strides). */
 };
 
 /* Dot epilogues.  A DOT whose aux2[0] = E > 0 is followed by E GEVO_OP_EXT

@@ -774,6 +774,23 @@ __device__ __noinline__ void run_tapsum(Shared& S, const gevo_instr& I) {
   __shared__ const double* tx[kTapMax];
   __shared__ const double* ty[kTapMax];
   __shared__ int sx[GEVO_MAXR], sy[GEVO_MAXR], so[GEVO_MAXR];
+  // epilogue micro-ops (aux2[3] of them, <= 3): sub | left << 4 in aux[m],
+  // operand m = EXT operand 2 * (ntap - 1) + m
+  constexpr int kTapEpi = 3;
+  const int nm = I.aux2[3];
+  __shared__ const double* mp[kTapEpi];
+  __shared__ int mst[kTapEpi][GEVO_MAXR];
+  if (threadIdx.x >= 32 && threadIdx.x < 32 + kTapEpi * GEVO_MAXR) {
+    const int m = (threadIdx.x - 32) / GEVO_MAXR, d = (threadIdx.x - 32) % GEVO_MAXR;
+    const int e = 2 * (ntap - 1) + m;
+    const gevo_operand& W = (&I)[1 + e / 3].in[e % 3];
+    if (m < nm) {
+      mst[m][d] = d < rank ? W.st[d] : 0;
+      if (d == 0) mp[m] = S.base[W.buf] + W.off;
+    } else {
+      mst[m][d] = 0;
+    }
+  }
   if (threadIdx.x < ntap) {
     const int t = threadIdx.x;
     const int ex = 2 * (t - 1), ey = ex + 1;      // operand index among the EXT records
@@ -795,22 +812,34 @@ __device__ __noinline__ void run_tapsum(Shared& S, const gevo_instr& I) {
   unravel(threadIdx.x, rank, I.shp, idx);
   unravel(kThreads, rank, I.shp, dig);
   __syncthreads();
+  int msub[kTapEpi], mleft[kTapEpi];
+#pragma unroll
+  for (int m = 0; m < kTapEpi; ++m) {
+    msub[m] = I.aux[m] & 15;
+    mleft[m] = (I.aux[m] >> 4) & 1;
+  }
   constexpr int U = 2;
   for (int base = threadIdx.x; base < n; base += U * kThreads) {
-    int ax[U], ay[U], ao[U];
+    int ax[U], ay[U], ao[U], am[U][kTapEpi];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      int a = 0, b = 0, c = 0;
+      int a = 0, b = 0, c = 0, w0 = 0, w1 = 0, w2 = 0;
 #pragma unroll
       for (int d = 0; d < GEVO_MAXR; ++d)
         if (d < rank) {
           a += idx[d] * sx[d];
           b += idx[d] * sy[d];
           c += idx[d] * so[d];
+          if (nm > 0) w0 += idx[d] * mst[0][d];
+          if (nm > 1) w1 += idx[d] * mst[1][d];
+          if (nm > 2) w2 += idx[d] * mst[2][d];
         }
       ax[u] = a;
       ay[u] = b;
       ao[u] = c;
+      am[u][0] = w0;
+      am[u][1] = w1;
+      am[u][2] = w2;
       int carry = 0;
 #pragma unroll
       for (int d = GEVO_MAXR - 1; d >= 0; --d) {
@@ -831,6 +860,17 @@ __device__ __noinline__ void run_tapsum(Shared& S, const gevo_instr& I) {
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (base + u * kThreads < n) v[u] = __dadd_rn(v[u], __dmul_rn(px[ax[u]], py[ay[u]]));
+    }
+#pragma unroll
+    for (int m = 0; m < kTapEpi; ++m) {
+      if (m < nm) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (base + u * kThreads < n) {
+            const double w = mp[m][am[u][m]];
+            v[u] = mleft[m] ? bin_f64(msub[m], v[u], w) : bin_f64(msub[m], w, v[u]);
+          }
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)

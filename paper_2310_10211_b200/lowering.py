@@ -45,6 +45,7 @@ KIND = {"f32": K_F64, "i32": K_I64, "i1": K_I1}
 OP_UNARY, OP_BINARY, OP_SELECT, OP_REDUCE, OP_DOT, OP_PAD, OP_EXT = 1, 2, 3, 4, 5, 6, 7
 OP_TAPSUM = 8          # sum of products, one pass (fuse_tap_sums, gevo_plan.h)
 TAP_MAX = 9
+TAP_EPI = 3            # binary micro-ops a TAPSUM may apply before its store
 EPI_SRC_OP = 64
 EPI_MAX_OPS = 8        # micro-ops fused into one dot epilogue
 EPI_MAX_EXT = 6        # extra operands (3 per continuation record)
@@ -703,6 +704,11 @@ def fuse_tap_sums(instrs):
             a, b = (muls if srcs[0] == muls[0] else muls[::-1])
             sums[j] = ([a, b], [a, b])
     drop = set()
+    busy = set(sums) | {i for _, ms in sums.values() for i in ms}
+    reader_of = {}
+    for alloc, rs in readers.items():
+        if len(rs) == 1:
+            reader_of[alloc] = rs[0]
     for j, (taps, members) in sums.items():
         xs = [instrs[i]["in"][0] for i in taps]
         ys = [instrs[i]["in"][1] for i in taps]
@@ -712,7 +718,28 @@ def fuse_tap_sums(instrs):
         rec["op"], rec["sub"] = OP_TAPSUM, len(taps)
         rec["in"] = [xs[0], ys[0]]
         rec["ext"] = [v for x, y in zip(xs[1:], ys[1:]) for v in (x, y)]
-        instrs[j] = rec
+        # epilogue: up to TAP_EPI single-use f64 binary consumers (the folded
+        # batch norm after a depthwise: * scale, + bias, max 0) become
+        # micro-ops applied before the store, each rounding as the op it
+        # replaces; the fused record takes the last consumer's place
+        micro, at, out = [], j, rec["out"]
+        while len(micro) < TAP_EPI and out.alloc >= 0 and out.buf == BUF_ARENA:
+            rr = reader_of.get(out.alloc)
+            if rr is None:
+                break
+            q, k = rr
+            r = instrs[q]
+            if q <= at or q in busy or not plain(r, r["sub"]) or r["sub"] > _B_MAX or \
+                    r["kout"] != K_F64 or k > 1 or not _same_view(r["in"][k], out) or \
+                    tuple(r["out"].shape) != tuple(out.shape):
+                break
+            micro.append((r["sub"], 1 if k == 0 else 0))
+            rec["ext"].append(r["in"][1 - k])
+            drop.add(at)
+            at, out = q, r["out"]
+        rec["micro"] = micro
+        rec["out"] = out
+        instrs[at] = rec
         drop.update(members)
     for i in sorted(drop, reverse=True):
         del instrs[i]
@@ -811,8 +838,13 @@ def encode_instrs(instrs, const_base=0) -> np.ndarray:
             exts = _ext_records({"ext": rec["ext"]})
             rec = dict(rec)
             aux2 = [0] * MAXR
-            aux2[4], aux2[5] = len(exts), rec["sub"]
+            micro = rec.get("micro", [])
+            aux2[3], aux2[4], aux2[5] = len(micro), len(exts), rec["sub"]
             rec["aux2"] = aux2
+            aux = [0] * MAXR
+            for m, (sub_, left) in enumerate(micro):
+                aux[m] = sub_ | (left << 4)
+            rec["aux"] = aux
             recs = [rec] + exts
         elif rec.get("epi"):
             exts = _ext_records(rec)

@@ -237,3 +237,5 @@ def test_fusion_changes_no_bit():
     assert nd > 0          # the CNN's BN chains fused
     taps = [r["sub"] for r in low.instrs if r["op"] == Lw.OP_TAPSUM]
     assert taps and all(t == 9 for t in taps)          # every depthwise 3x3 is one TAPSUM
+    micro = [len(r.get("micro", [])) for r in low.instrs if r["op"] == Lw.OP_TAPSUM]
+    assert all(m == 3 for m in micro)                  # ... with its BN (*, +, max) as micro-ops

@@ -124,12 +124,17 @@ def run(instrs, mem):
                 if rec.get("epi"):
                     r = apply_epilogue(mem, rec, r)
             elif op == Lw.OP_TAPSUM:
-                xs = [rec["in"][0]] + rec["ext"][0::2]
-                ys = [rec["in"][1]] + rec["ext"][1::2]
+                nt = rec["sub"]
+                taps = rec["ext"][:2 * (nt - 1)]
+                xs = [rec["in"][0]] + taps[0::2]
+                ys = [rec["in"][1]] + taps[1::2]
                 v = fl(gather(mem, xs[0], shape)) * fl(gather(mem, ys[0], shape))
                 for x, y in zip(xs[1:], ys[1:]):
                     v = v + fl(gather(mem, x, shape)) * fl(gather(mem, y, shape))
                 r = wd(v)
+                for (msub, left), w in zip(rec.get("micro", []), rec["ext"][2 * (nt - 1):]):
+                    wv = gather(mem, w, shape)
+                    r = ew(Lw.OP_BINARY, msub, F, F, [r, wv] if left else [wv, r])
             elif op == Lw.OP_PAD:
                 a, pv = rec["in"]
                 low, ext_ = rec["aux"][:len(shape)], rec["aux2"][:len(shape)]
