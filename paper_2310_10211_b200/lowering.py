@@ -746,6 +746,41 @@ def fuse_tap_sums(instrs):
     return instrs
 
 
+def mem_order_elementwise(instrs):
+    """Walk plain elementwise instructions in their output's memory order.
+
+    An elementwise op is the same per element in any index order, so its
+    dims may be permuted consistently across the output and every operand.
+    When the output is a dense block in some other dim order (e.g. a
+    column-major 784 x 32 weight returned by a variant whose steps flip
+    layouts), sorting the dims by the output's strides makes the output --
+    and every operand laid out like it -- a linear, coalesced stream instead
+    of a row walk with a 784-element stride."""
+    for i, r in enumerate(instrs):
+        if r["op"] not in _EW_OPS or r.get("epi") or r.get("ext"):
+            continue
+        out = r["out"]
+        shape, st = tuple(out.shape), tuple(out.st)
+        if len(shape) < 2:
+            continue
+        perm = sorted(range(len(shape)), key=lambda d: (-st[d], d))
+        if perm == list(range(len(shape))):
+            continue
+        pshape = tuple(shape[d] for d in perm)
+        pst = tuple(st[d] for d in perm)
+        if any(a != b for a, b, e in zip(pst, L.c_strides(pshape), pshape) if e != 1):
+            continue
+
+        def permuted(v):
+            return Val(v.buf, v.off, pshape, tuple(v.st[d] for d in perm), v.kind, v.alloc)
+        new = dict(r)
+        new["out"] = permuted(out)
+        new["in"] = [permuted(v) for v in r["in"]]
+        new["shp"] = _pad_dims(pshape)
+        instrs[i] = new
+    return instrs
+
+
 def lower_function(fn, param_layouts=None, ret_bufs=None, ret_layout="compact",
                    cost_table=None, smem_budget=None, fuse=True) -> Lowered:
     """Lower one function.  Params i live in buffer PARAM0+i with the given
@@ -764,6 +799,7 @@ def lower_function(fn, param_layouts=None, ret_bufs=None, ret_layout="compact",
         fuse_dot_epilogues(b.instrs)
         fuse_tap_sums(b.instrs)
         fuse_ew_chains(b.instrs)
+    mem_order_elementwise(b.instrs)
     top, stop = b.assign_arena(smem_budget)
     # resolve arena offsets into the operands
     instrs = []
