@@ -239,3 +239,24 @@ def test_fusion_changes_no_bit():
     assert taps and all(t == 9 for t in taps)          # every depthwise 3x3 is one TAPSUM
     micro = [len(r.get("micro", [])) for r in low.instrs if r["op"] == Lw.OP_TAPSUM]
     assert all(m == 3 for m in micro)                  # ... with its BN (*, +, max) as micro-ops
+
+
+def test_elementwise_walks_output_memory_order():
+    """A copy between two column-major 784 x 32 blocks (a variant returning a
+    transposed view in the layout its next step reads) is walked in memory
+    order: both sides linear, and the emulated result is unchanged."""
+    fn = dialect.parse_function(
+        "func @f(%a: tensor<32x784xf32>, %b: tensor<32x784xf32>) -> tensor<784x32xf32> {\n"
+        "  %t = transpose %a {perm = [1, 0]} : tensor<784x32xf32>\n"
+        "  %u = transpose %b {perm = [1, 0]} : tensor<784x32xf32>\n"
+        "  %s = add %t, %u : tensor<784x32xf32>\n"
+        "  return %s : tensor<784x32xf32>\n}")
+    rng = np.random.default_rng(3)
+    a, b = rng.standard_normal((32, 784)), rng.standard_normal((32, 784))
+    low = Lw.lower_function(fn, None, ret_layout="compact")
+    (rec,) = [r for r in low.instrs if r["op"] == Lw.OP_BINARY]
+    assert tuple(rec["out"].shape) == (32, 784)              # dims in memory order
+    assert Lw._addr_mode(rec["out"], (32, 784)) == Lw.AM_LINEAR
+    assert all(Lw._addr_mode(v, (32, 784)) == Lw.AM_LINEAR for v in rec["in"])
+    (got,), _ = emulate(fn, [a, b])
+    assert np.array_equal(got, (a.T + b.T))
