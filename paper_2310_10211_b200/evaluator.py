@@ -234,24 +234,41 @@ class DeviceEvaluator:
                     slots.append(i)
             if not lowered:
                 continue
-            wts = [device_weight(v, cfg.steps if training else 0, n_score) for v in lowered]
-            parts = 1 if training else self.score_parts(lowered, n_score, len(idx))
-            if parts > 1:
-                order = np.argsort(-np.asarray(wts), kind="stable")
-            else:
-                layout = self._sm_layout.get(len(lowered))
-                order = layout_order(wts, layout) if layout else sm_aware_order(wts, self.n_sms)
-            plan = build_population_plan(lowered, self.weight_shapes, self.batch * self.classes,
-                                         order=order, parts=parts)
+            # launches of this half: one, unless the individuals' device
+            # scratch exceeds the budget (a large CNN population), then
+            # consecutive groups that each fit, run one after another
+            groups = self._scratch_groups(lowered, len(halves))
+            plans = []
+            for g0, g1 in groups:
+                gl = lowered[g0:g1]
+                wts = [device_weight(v, cfg.steps if training else 0, n_score) for v in gl]
+                parts = 1 if training else self.score_parts(gl, n_score, len(idx) if len(groups) == 1 else None,
+                                                            shares=len(halves))
+                if parts > 1:
+                    order = np.argsort(-np.asarray(wts), kind="stable")
+                else:
+                    layout = self._sm_layout.get(len(gl))
+                    order = layout_order(wts, layout) if layout else sm_aware_order(wts, self.n_sms)
+                plan = build_population_plan(gl, self.weight_shapes, self.batch * self.classes,
+                                             order=order, parts=parts)
+                plan_bytes += plan.blob.nbytes
+                plans.append((plan, order if parts == 1 and len(groups) == 1 else None, g1 - g0))
             tc = time.perf_counter()
             t_lower += tb - ta
             t_pack += tc - tb
-            plan_bytes += plan.blob.nbytes
-            args = (plan.blob, plan.n_prog, 0 if training else 1, cfg.steps if training else 0,
-                    cfg.finite_check_every, SPLIT_SEARCH, split, self.weight_elems, want_weights)
+            mode_args = (0 if training else 1, cfg.steps if training else 0,
+                         cfg.finite_check_every, SPLIT_SEARCH, split, self.weight_elems, want_weights)
 
-            def run(c=ctxs[h], a=args, key=h, lv=lowered, sl=slots, od=order if parts == 1 else None):
-                box[key] = (c.eval(*a), lv, sl, od)
+            def run(c=ctxs[h], pl=plans, ma=mode_args, key=h, lv=lowered, sl=slots):
+                recs, fws, od = [], [], None
+                for plan, order_, n_g in pl:
+                    res, fw = c.eval(plan.blob, plan.n_prog, *ma)
+                    recs.append(res[:n_g])
+                    fws.append(fw[:n_g] if fw is not None else None)
+                    od = order_
+                res = np.concatenate(recs)
+                fw = np.concatenate(fws) if fws and fws[0] is not None else None
+                box[key] = ((res, fw), lv, sl, od)
             if h + 1 < len(jobs):
                 import threading
                 runner = threading.Thread(target=run)
@@ -293,7 +310,23 @@ class DeviceEvaluator:
             out.append(finals)
         return out[0] if len(out) == 1 else tuple(out)
 
-    def score_parts(self, lowered, n_score, n_total=None):
+    def _scratch_groups(self, lowered, shares=1):
+        """[g0, g1) ranges of `lowered` whose device scratch (arena, probs
+        and weight ping-pong per individual) fits GEVO_B200_ARENA_GB (default
+        64) split over `shares` concurrent launches."""
+        budget = float(os.environ.get("GEVO_B200_ARENA_GB", "64")) * 1e9 / max(1, shares)
+        fixed = 8 * (((self.batch * self.classes + 15) & ~15) + 2 * ((self.weight_elems + 15) & ~15))
+        groups, g0, acc = [], 0, 0
+        for k, v in enumerate(lowered):
+            b = 8 * ((v.arena + 15) & ~15) + fixed
+            if k > g0 and acc + b > budget:
+                groups.append((g0, k))
+                g0, acc = k, 0
+            acc += b
+        groups.append((g0, len(lowered)))
+        return groups
+
+    def score_parts(self, lowered, n_score, n_total=None, shares=1):
         """Programs per prediction-mode individual (plan.build_population_plan
         `parts`): enough to give the launch two CTAs per SM, at most one per
         scored batch, and within GEVO_B200_ARENA_GB (default 64) of scratch.
@@ -308,7 +341,7 @@ class DeviceEvaluator:
         parts = max(1, min(n_score, (2 * self.n_sms) // max(n, n_total or 0)))
         per = sum(8 * ((v.arena + 15) & ~15) for v in lowered) + \
             8 * n * (self.batch * self.classes + 2 * self.weight_elems + 48)
-        budget = float(os.environ.get("GEVO_B200_ARENA_GB", "64")) * 1e9
+        budget = float(os.environ.get("GEVO_B200_ARENA_GB", "64")) * 1e9 / max(1, shares)
         while parts > 1 and parts * per > budget:
             parts -= 1
         return parts

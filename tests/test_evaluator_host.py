@@ -199,3 +199,23 @@ def test_prediction_score_parts_cover_every_batch_once(monkeypatch, n, forced):
         assert f.error == r["wrong"] / r["total"]
     assert bad == sum(len(c.plans) for c in FakeContext.instances)  # slot 3 of each launch
     ev.close()
+
+
+def test_scratch_budget_splits_a_half_into_sequential_launches(fake, monkeypatch):
+    """Individuals whose device scratch exceeds GEVO_B200_ARENA_GB run as
+    consecutive launches that each fit; results still map to their variants."""
+    wl = W.build_2fcnet_workload(W.WorkloadConfig(steps=60, dataset=W.DatasetConfig(
+        search_n=320, holdout_n=64)))
+    inds = load("train_pop.json.gz")["individuals"][:20]
+    variants = [variant_functions(i) for i in inds]
+    monkeypatch.setenv("GEVO_B200_ARENA_GB", "0.002")       # ~2 MB: a few individuals per launch
+    ev = E.DeviceEvaluator(wl)
+    fits, recs = ev.evaluate_variants(variants, return_records=True)
+    plans = [p for c in fake.instances for p in c.plans]
+    assert len(plans) > 2 and sum(plans) == len(variants)
+    for f, r in zip(fits, recs):
+        if r["status"] != E.STATUS_OK:
+            assert f.error == 1.0
+        else:
+            assert f.error == r["wrong"] / 992
+    ev.close()
