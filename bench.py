@@ -1,26 +1,32 @@
 """Benchmark: fresh individuals evaluated per second (BASELINE.json metric).
 
 Workload (BASELINE.json configs[1]): train2fc (784-32-10 MLP, 600 SGD steps
-+ 31 scored batches per individual) on synthetic MNIST-shaped data; a step
-evaluates one population of 256 fresh mutated individuals per GPU, drawn
-from a recorded seeded GA run (pop 256 x 10 generations, tests/golden/
-bench_train_pool.json.gz) -- real variant programs, not copies of one.
++ 31 scored batches per individual) on synthetic MNIST-shaped data.  A step
+evaluates one population of `--pop` (default 256) fresh mutated individuals,
+drawn from a recorded seeded GA run (pop 256 x 10 generations,
+tests/golden/bench_train_pool.json.gz): real patches of the reference's
+genome, not copies of one program.  With N GPUs the same population is
+sharded over the ranks (strong scaling: configs[1] is "population 256 ...
+sharded over 8xB200").
 
-  value  = individuals / device time of the evaluation kernels (inputs and
-           plans resident; CUDA events on the launching stream, max over
-           ranks)
-  e2e    = individuals / wall time of the public API call
-           DeviceEvaluator.evaluate_variants (host lowering in a process
-           pool, overlapped with the device: half the generation runs while
-           the other half is lowered; plan H2D + kernels + result D2H), plus
-           the record all-gather when N > 1
+  value  = individuals / device time of the evaluation kernels (plans
+           resident; CUDA events on the launching stream; max over ranks)
+  e2e    = individuals / wall time of the reference's own seam,
+           evotir.search._Evaluator(workload)(patches) with
+           shims.install() (search.py:257-273): patch_dumps keys, apply_patch
+           + verify + lowering in the worker processes, plan H2D, kernels,
+           result D2H, and the NCCL record all-gather when N > 1
+  cnn    = BASELINE.json configs[2] (MobileNetV2-CIFAR width 0.5, 128
+           reference-made mutants) on a bounded 1 000-image sample
 
-`--impl reference` times the reference's algorithm on the host CPU (the
-oracle port, all cores, process pool), on the same workload.
+`--impl reference` times the UNMODIFIED reference (baseline/_ref, installed by
+baseline/install_ref.sh): evotir.fitness.evaluate over the same patches in a
+process pool on every host core.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -35,7 +41,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 POP = 256
 METRIC = "individuals evaluated/sec per generation"
 UNIT = "individuals/s"
-WORKLOAD = "train2fc pop256 (784-32-10 MLP, 600 SGD steps + 31 scored batches, synthetic MNIST-shaped)"
+WORKLOAD = "train2fc (784-32-10 MLP, 600 SGD steps + 31 scored batches, synthetic MNIST-shaped)"
 
 
 def parse_args():
@@ -44,8 +50,10 @@ def parse_args():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--pop", type=int, default=POP)
+    p.add_argument("--pop", type=int, default=POP, help="population per step (whole job)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-cnn", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
 
 
@@ -143,48 +151,60 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_eval_one(args):
-    fns_text, kind = args
-    from oracle import fitness as OF
-    from paper_2310_10211_b200 import workloads as W
-    from paper_2310_10211_b200.dialect import parse_function
-    global _WL
-    if "_WL" not in globals() or _WL is None:
-        _WL = W.build_2fcnet_workload()
-    wl = _WL
-    fns = {k: parse_function(v) for k, v in fns_text.items()}
-    w0 = [wl.weights[n] for n in W.WEIGHT_NAMES]
-    return OF.evaluate_variant(fns, "training", w0,
-                               (wl.search_x, wl.search_y, wl.search_labels))
+# ---------------------------------------------------------------------------
+# the reference itself on the host CPU (baseline/_ref)
+# ---------------------------------------------------------------------------
+
+_REF_WL = None
 
 
-_WL = None
+def _need_reference():
+    from golden_io import reference_available
+    if not reference_available():
+        raise SystemExit("the reference (evotir) is not importable: run baseline/install_ref.sh")
 
 
-def cpu_throughput(inds, seconds_budget=15.0):
-    """The reference algorithm (oracle port: same numpy calls as
-    interpreter.py/fitness.py) on all host cores, one process per core,
-    OPENBLAS_NUM_THREADS=1 (results identical to serial)."""
+def _ref_eval(key):
+    """One unmodified evotir.fitness.evaluate (fitness.py:372-393) of a patch."""
+    from evotir import fitness as F
+    from evotir.genome import patch_loads
+    f = F.evaluate(_REF_WL.module, patch_loads(key), _REF_WL)
+    return f.cost, f.error, f.valid
+
+
+def reference_throughput(keys, seconds=None):
+    """evotir.fitness.evaluate over `keys` in a process pool with one process
+    per host core and OPENBLAS_NUM_THREADS=1 (the reference's own thread pool
+    is slower than serial).  With `seconds`, a bounded sample:
+    as many keys as the warm pool gets through in about that time.  Returns
+    (individuals/s, cores, n, seconds, results)."""
+    global _REF_WL
     import multiprocessing as mp
-    cores = os.cpu_count() or 1
+    _need_reference()
+    from evotir import fitness as F
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    n = max(cores, min(len(inds), int(cores * seconds_budget / 0.3)))
-    n = min(n, len(inds))
-    work = [({k: i[k] for k in ("forward", "train_step")}, "training") for i in inds[:n]]
+    cores = os.cpu_count() or 1
+    if _REF_WL is None:
+        _REF_WL = F.build_2fcnet_workload()          # inherited by the forked workers
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        pool.map(cpu_eval_one, work[:cores])     # warm workers
         t = time.perf_counter()
-        pool.map(cpu_eval_one, work, chunksize=1)
+        pool.map(_ref_eval, keys[:cores], chunksize=1)      # warm every worker
+        warm = time.perf_counter() - t
+        n = len(keys)
+        if seconds is not None:
+            n = max(cores, min(len(keys), int(cores * seconds / max(warm, 1e-3))))
+        t = time.perf_counter()
+        res = pool.map(_ref_eval, keys[:n], chunksize=1)
         dt = time.perf_counter() - t
-    return n / dt, cores, n, dt
+    return n / dt, cores, n, dt, res
 
 
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 and args.impl != "reference":
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -193,29 +213,98 @@ def dist_setup(args):
 
 
 def run_reference(args, world, rank):
+    """The reference arm: rank 0 alone, every host core."""
     if rank != 0:
         return
     inds, _ = load_pool()
-    rates = []
-    cores = os.cpu_count() or 1
+    rates, ns, cores = [], [], os.cpu_count() or 1
+    per_step = None
     for s in range(args.warmup + args.steps):
-        r, cores, n, dt = cpu_throughput(inds[(s * 7) % max(1, len(inds) - 64):], 8.0)
+        start = (s * args.pop) % len(inds)
+        keys = [inds[(start + k) % len(inds)]["key"] for k in range(args.pop)]
+        if per_step is None:
+            # size the sample once so the whole run stays within minutes
+            r, cores, n, dt, _ = reference_throughput(keys, seconds=4.0)
+            per_step = n
+        else:
+            r, cores, n, dt, _ = reference_throughput(keys[:per_step])
         if s >= args.warmup:
             rates.append(r)
+            ns.append(n)
     value = statistics.median(rates)
+    sample = (f"{ns[0]} of the {args.pop} fresh patches of each step "
+              f"(bench pool, seeded GA), evotir.fitness.evaluate on {cores} processes")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * args.pop / value, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "population": args.pop,
-                       "sample": f"{n} individuals per step on {cores} processes"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores,
-                             "kind": "port",
-                             "sample": f"{n} fresh individuals of the bench pool per step, "
-                                       "oracle/ numpy restatement (bit-identical to the reference)"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "population": args.pop, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                             "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+
+def lib_sha():
+    from paper_2310_10211_b200 import _lib
+    with open(_lib.LIB_PATH, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()[:16]
+
+
+def measured_traffic(sha):
+    """ncu dram bytes of the hot kernel per launch, recorded by
+    tests/tools/ncu_traffic.py for THIS build of libgevo.so (profiles/
+    traffic.json carries the sha of the library it measured); null when the
+    capture is of another build."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except (OSError, ValueError):
+        return None, None
+    if t.get("lib_sha") != sha:
+        return None, None
+    return t.get("dram_bytes_per_launch"), t
+
+
+def cnn_measure(local, steps=1):
+    """configs[2] on a bounded sample: the 16 reference-made mutants of the
+    full network (tests/golden/cnn_full_pop.json.gz) x 8 = population 128,
+    scored over 1 000 synthetic CIFAR-shaped images (batch 100)."""
+    from golden_io import load
+    from paper_2310_10211_b200 import cnn, dialect
+    from paper_2310_10211_b200.evaluator import DeviceEvaluator
+    g = load("cnn_full_pop.json.gz")
+    n_img, batch = 1000, 100
+    cfg = cnn.CnnConfig(**cnn.MOBILENETV2_CIFAR_HALF, batch_size=batch, search_n=n_img,
+                        holdout_n=batch)
+    wl = cnn.build_cnn_prediction_workload(cfg)
+    base = [{"forward": dialect.parse_function(i["forward"])} for i in g["individuals"]]
+    variants = [base[k % len(base)] for k in range(128)]
+    fn = base[0]["forward"]
+    macs, types = 0, dict(fn.params)
+    for op in fn.ops:
+        if op.opcode == "dot":
+            a, b = types[op.operands[0]], types[op.operands[1]]
+            macs += a.shape[0] * a.shape[1] * b.shape[1]
+        types[op.result] = op.result_type
+    ev = DeviceEvaluator(wl, device=local)
+    ev.evaluate_variants(variants)                      # warm-up
+    dev, wall = [], []
+    for _ in range(steps):
+        t = time.perf_counter()
+        fits = ev.evaluate_variants(variants)
+        wall.append(time.perf_counter() - t)
+        dev.append(ev.last_device_ms / 1e3)
+    ev.close()
+    d, w = statistics.median(dev), statistics.median(wall)
+    return {"workload": "configs[2]: MobileNetV2-CIFAR width 0.5, population 128 "
+                        "(16 reference-made mutants x 8), bounded sample of 1000 images "
+                        "(batch 100) of the 10k-image split",
+            "value": 128 / d, "unit": UNIT, "images_per_s": 128 * n_img / d,
+            "e2e": 128 / w, "fp64_dot_tflops": 2.0 * macs * (n_img // batch) * 128 / d / 1e12,
+            "ms_per_step": 1e3 * d, "statuses_ok": sum(f.error < 1.0 for f in fits)}
 
 
 def main():
@@ -227,22 +316,20 @@ def main():
     import numpy as np
     import torch
     from paper_2310_10211_b200 import workloads as W
-    from paper_2310_10211_b200.evaluator import DeviceEvaluator
-    from paper_2310_10211_b200 import distributed as D
+    from paper_2310_10211_b200.evaluator import DeviceEvaluator, lower_all
+    from paper_2310_10211_b200.plan import (build_population_plan, device_weight, layout_order,
+                                            sm_aware_order)
 
     torch.cuda.set_device(local)
     inds, parse_function = load_pool()
     wl = W.build_2fcnet_workload()
     ev = DeviceEvaluator(wl, device=local)
     total_steps = args.warmup + args.steps
-    # distinct individuals per (rank, step) where the pool allows
-    stride = args.pop
-    def batch_for(s):
-        start = ((s * world + rank) * stride) % len(inds)
-        sel = [inds[(start + k) % len(inds)] for k in range(args.pop)]
-        return sel, [{n: parse_function(i[n]) for n in ("forward", "train_step")} for i in sel]
 
-    batches = [batch_for(s) for s in range(total_steps)]
+    def pop_for(s):
+        start = (s * args.pop) % len(inds)
+        return [inds[(start + k) % len(inds)] for k in range(args.pop)]
+    pops = [pop_for(s) for s in range(total_steps)]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     nb = wl.n_search_batches
     steps_cfg = wl.config.steps
@@ -254,22 +341,18 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    kern_ms, wall_s, alg_bytes, alg_flops, h2d, d2h = [], [], [], [], [], []
-    parity_ok = parity_n = 0
-    from paper_2310_10211_b200.evaluator import lower_all
-    from paper_2310_10211_b200.plan import build_population_plan
     clocks = Clocks(local)
-    # (1) value: plans built before timing; one launch per step on one
-    # context; device time of the evaluation kernel (CUDA events)
-    lowered_steps = []
+    # (1) value: this rank's shard (strided, as the seam shards it), lowered
+    # before timing; one launch per step; device time (CUDA events)
+    kern_ms, alg_bytes, alg_flops = [], [], []
+    shard_steps = []
     for s in range(total_steps):
-        lowered_steps.append([v for v in lower_all(batches[s][1], wl.config.cost_table, True, steps_cfg)
-                              if v is not None])
-    from paper_2310_10211_b200.plan import device_weight, layout_order, sm_aware_order
+        mine = pops[s][rank::world]
+        fns = [{n: parse_function(i[n]) for n in ("forward", "train_step")} for i in mine]
+        shard_steps.append((fns, [v for v in lower_all(fns, wl.config.cost_table, True, steps_cfg)
+                                  if v is not None]))
     for s in range(total_steps):
-        sel, fns = batches[s]
-        vps = lowered_steps[s]
-        # launch order from the block -> SM layout the previous launch showed
+        fns, vps = shard_steps[s]
         wts = [device_weight(v, steps_cfg, nb) for v in vps]
         layout = ev._sm_layout.get(len(vps))
         order = layout_order(wts, layout) if layout else sm_aware_order(wts, ev.n_sms)
@@ -285,38 +368,50 @@ def main():
             kern_ms.append(ev.ctx.last_kernel_ms())
             alg_bytes.append(sum(per_individual_bytes(f, steps_cfg, nb) for f in fns))
             alg_flops.append(sum(per_individual_flops(f, steps_cfg, nb) for f in fns))
-    # (2) e2e: the public call on host data (lowering, plan H2D, kernels,
-    # results D2H; the record all-gather when N > 1), wall clock
-    for s in range(total_steps):
-        sel, fns = batches[s]
-        flush.zero_()
-        barrier()
-        t0 = time.perf_counter()
-        fits, recs = ev.evaluate_variants(fns, return_records=True)
-        if world > 1:
-            loc = D.pack_records(fits, recs)
-            D.all_gather_records(loc, args.pop)
-        t1 = time.perf_counter()
-        if s >= args.warmup:
-            wall_s.append(t1 - t0)
-            h2d.append(int(ev.last_plan_bytes))
-            d2h.append(args.pop * 24)
-            # the pool records the reference's own fitness for every variant
-            for f, ind in zip(fits, sel):
-                parity_n += 1
-                parity_ok += (f.cost, f.error) == (ind["cost"], ind["error"])
+    # (2) e2e through the reference's seam: _Evaluator(workload)(patches)
+    wall_s, h2d, d2h, e2e_launches = [], [], [], 0
+    parity_ok = parity_n = 0
+    if not args.no_e2e:
+        _need_reference()
+        import evotir.search as S
+        from evotir import fitness as F
+        from evotir.genome import patch_loads
+        from paper_2310_10211_b200 import shims
+        rwl = F.build_2fcnet_workload()
+        shims.install(device=local)
+        patches = [[patch_loads(i["key"]) for i in pops[s]] for s in range(total_steps)]
+        dev = shims.device_for(rwl, local)
+        for s in range(total_steps):
+            E = S._Evaluator(rwl)                   # fresh cache: every patch is evaluated
+            flush.zero_()
+            barrier()
+            n0 = dev.launches
+            t0 = time.perf_counter()
+            fits = E(patches[s])
+            t1 = time.perf_counter()
+            if s >= args.warmup:
+                wall_s.append(t1 - t0)
+                e2e_launches += dev.launches - n0
+                h2d.append(int(dev.last_plan_bytes))
+                # records of this rank's shard + the gathered records
+                n_mine = len(pops[s][rank::world])
+                d2h.append(n_mine * 56 + (args.pop * 32 + 32 * world if world > 1 else 0))
+                for f, ind in zip(fits, pops[s]):
+                    parity_n += 1
+                    parity_ok += (f.cost, f.error) == (ind["cost"], ind["error"])
+        shims.uninstall()
     barrier()
     ck = clocks.stop()
     dev_s = sum(kern_ms) / 1000.0
-    e2e_s = sum(wall_s)
+    e2e_s = sum(wall_s) if wall_s else float("nan")
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([dev_s, e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_s, e2e_s = t.tolist()
-    n_total = args.pop * args.steps * world
+    n_total = args.pop * args.steps
     value = n_total / dev_s
-    e2e = n_total / e2e_s
+    e2e = n_total / e2e_s if wall_s else None
     if rank == 0:
         peaks = {}
         try:
@@ -327,41 +422,52 @@ def main():
         per_launch_bytes = statistics.mean(alg_bytes)
         per_launch_s = statistics.mean(kern_ms) / 1000.0
         achieved = per_launch_bytes / per_launch_s / 1e9
-        traffic = None
-        try:
-            traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(
-                "dram_bytes_per_launch")
-        except OSError:
-            pass
+        sha = lib_sha()
+        traffic, tinfo = measured_traffic(sha)
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            r, cores, n, dt = cpu_throughput(inds, 10.0)
-            cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port",
-                   "sample": f"{n} individuals of the bench pool, oracle/ numpy restatement "
-                             f"on {cores} processes ({dt:.1f} s)"}
+            try:
+                r, cores, n, dt, _ = reference_throughput([i["key"] for i in pops[0]], 10.0)
+                cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "reference",
+                       "sample": f"{n} fresh patches of the bench population, unmodified "
+                                 f"evotir.fitness.evaluate (baseline/_ref) on {cores} "
+                                 f"processes ({dt:.1f} s)"}
+            except SystemExit as e:
+                cpu = {"value": None, "unavailable": str(e)}
+        cnn_line = None
+        if not args.no_cnn and world == 1:
+            cnn_line = cnn_measure(local)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * dev_s / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded synthetic_digits, recorded GA variants)",
-            "config": {"workload": WORKLOAD, "population_per_gpu": args.pop,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded synthetic_digits, recorded GA patches)",
+            "config": {"workload": f"{WORKLOAD}, population {args.pop}",
+                       "population": args.pop, "population_per_gpu": args.pop / world,
                        "steps_per_individual": steps_cfg, "scored_batches": nb,
                        "l2": "flushed between timed iterations (256 MB write)",
-                       "parallelism": f"population sharded, {world} GPU(s), records all-gathered"},
+                       "parallelism": f"population sharded over {world} GPU(s), "
+                                      "records all-gathered (gevo_allgather, NCCL)"},
             "e2e": {"value": e2e, "unit": UNIT,
-                    "h2d_bytes_per_step": int(statistics.mean(h2d)),
-                    "d2h_bytes_per_step": int(statistics.mean(d2h))},
-            "gpu_launches": args.steps,
+                    "h2d_bytes_per_step": int(statistics.mean(h2d)) if h2d else None,
+                    "d2h_bytes_per_step": int(statistics.mean(d2h)) if d2h else None,
+                    "seam": "evotir.search._Evaluator(workload)(patches) with shims.install()",
+                    "launches": e2e_launches},
+            "gpu_launches": len(kern_ms),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
+                         "traffic_source": (tinfo or {}).get("source"),
                          "algorithmic_bytes_per_launch": per_launch_bytes,
-                         "fp64_tflops": statistics.mean(alg_flops) / per_launch_s / 1e12},
+                         "fp64_tflops": statistics.mean(alg_flops) / per_launch_s / 1e12,
+                         "lib_sha": sha},
             "cpu_baseline": cpu,
             "clocks": ck,
             "parity": {"bit_exact": parity_ok, "of": parity_n,
                        "against": "reference (cost, error) recorded in the bench pool"},
         }
+        if cnn_line is not None:
+            line["cnn"] = cnn_line
         print(json.dumps(line), flush=True)
     ev.close()
     if world > 1:

@@ -32,6 +32,13 @@
  *   gevo_archive_merge           -- Archive.offer (search.py:208-228) for a
  *                                   batch of offers with new keys
  *   gevo_hypervolume             -- hypervolume (search.py:182-195)
+ *   gevo_comm_unique_id /        -- (no reference analogue: the reference is
+ *   gevo_comm_init /                single-process) one NCCL communicator per
+ *   gevo_allgather /                context; ONE all-gather of fixed-size
+ *   gevo_comm_destroy               fitness records per generation after each
+ *                                   rank evaluated its shard of the fresh
+ *                                   patches of _Evaluator.__call__
+ *                                   (search.py:257-273), SURVEY.md §8(e)
  *   gevo_last_error              -- (Python exceptions in the reference)
  *   gevo_profile                 -- (no analogue: per-instruction-class
  *                                   cycle counters for diagnostics)
@@ -65,7 +72,8 @@ enum {
   GEVO_E_ARG = -1,      /* bad argument / malformed plan */
   GEVO_E_CUDA = -2,     /* CUDA runtime failure */
   GEVO_E_NOSPLIT = -3,  /* split id not uploaded */
-  GEVO_E_STATE = -4     /* weights not uploaded, ... */
+  GEVO_E_STATE = -4,    /* weights not uploaded, ... */
+  GEVO_E_COMM = -5      /* NCCL unavailable or failed */
 };
 
 /* per-individual status: the reference's failure encodings (fitness.py:
@@ -194,6 +202,17 @@ int gevo_last_kernel_ms(gevo_ctx* ctx, double* ms);
  * of the later of the two contexts' last gevo_eval (one generation split in
  * two halves over two contexts/streams of the same device) */
 int gevo_span_ms(gevo_ctx* first, gevo_ctx* second, double* ms);
+
+/* NCCL plumbing for population sharding (NCCL is dlopen'ed on first use).
+ * gevo_comm_unique_id writes an ncclUniqueId (128 bytes; len >= 128) that
+ * rank 0 creates and every rank passes to gevo_comm_init.  gevo_allgather
+ * copies `bytes` from host `send`, all-gathers them over the context's
+ * communicator on its stream (NVLink/NVSwitch between the GPUs of a node)
+ * and writes world * bytes, rank-major, to host `recv`. */
+int gevo_comm_unique_id(void* out, size_t len);
+int gevo_comm_init(gevo_ctx* ctx, int rank, int world, const void* uid, size_t len);
+int gevo_allgather(gevo_ctx* ctx, const void* send, size_t bytes, void* recv);
+int gevo_comm_destroy(gevo_ctx* ctx);
 
 /* device and build info, e.g. "NVIDIA B200 sm_100 148 SMs" */
 int gevo_device_info(gevo_ctx* ctx, char* buf, size_t len);

@@ -106,7 +106,8 @@ typedef struct {
 } gevo_instr;                         /* 224 bytes */
 
 /* gevo_prog.flags */
-#define GEVO_FLAG_LAYOUT_APPROX 1     /* returned layouts had no period <= 2 */
+/* bit 0 is unused: a variant whose returned layouts have no period <= 2 is
+ * refused by the lowering (plan.UnsupportedVariant), never approximated */
 #define GEVO_FLAG_ALTERNATE 2         /* steps >= 1: odd -> train1, even -> train0 */
 /* Score parts (prediction mode only): an individual's scored batches are
  * independent (fitness.py:361-368), so n_parts programs may share one

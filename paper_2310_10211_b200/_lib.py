@@ -77,7 +77,25 @@ SIGNATURES = {
                                           c_i32p, c_i32p]),
     "gevo_hypervolume": (ctypes.c_int, [ctypes.c_void_p, c_dblp, c_dblp, ctypes.c_int,
                                         ctypes.c_double, ctypes.c_double, c_dblp]),
+    "gevo_comm_unique_id": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t]),
+    "gevo_comm_init": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_void_p, ctypes.c_size_t]),
+    "gevo_allgather": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                      ctypes.c_void_p]),
+    "gevo_comm_destroy": (ctypes.c_int, [ctypes.c_void_p]),
 }
+
+NCCL_UID_BYTES = 128
+
+
+def comm_unique_id() -> bytes:
+    """An ncclUniqueId from libgevo (rank 0 creates it, every rank passes it
+    to Context.comm_init)."""
+    buf = ctypes.create_string_buffer(NCCL_UID_BYTES)
+    rc = load().gevo_comm_unique_id(buf, NCCL_UID_BYTES)
+    if rc != 0:
+        raise GevoError(f"gevo_comm_unique_id failed (rc={rc}): NCCL unavailable")
+    return buf.raw
 
 _lib = None
 
@@ -123,6 +141,7 @@ class Context:
 
     def __init__(self, device: int = 0):
         self.lib = load()
+        self.device = device
         h = ctypes.c_void_p()
         rc = self.lib.gevo_create(device, ctypes.byref(h))
         self.h = h
@@ -284,6 +303,23 @@ class Context:
                                                ptr(keep, ctypes.c_int32), ctypes.byref(nk)),
                    "archive_merge")
         return keep[:nk.value]
+
+    def comm_init(self, rank: int, world: int, uid: bytes):
+        buf = ctypes.create_string_buffer(bytes(uid), NCCL_UID_BYTES)
+        self.check(self.lib.gevo_comm_init(self.h, rank, world, buf, NCCL_UID_BYTES),
+                   "gevo_comm_init")
+
+    def allgather(self, send: np.ndarray, world: int) -> np.ndarray:
+        """All-gather `send` (any dtype, same size on every rank) over the
+        context's NCCL communicator: returns [world, *send.shape]."""
+        send = np.ascontiguousarray(send)
+        out = np.empty((world,) + send.shape, dtype=send.dtype)
+        self.check(self.lib.gevo_allgather(self.h, send.ctypes.data, send.nbytes,
+                                           out.ctypes.data), "gevo_allgather")
+        return out
+
+    def comm_destroy(self):
+        self.check(self.lib.gevo_comm_destroy(self.h), "gevo_comm_destroy")
 
     def hypervolume(self, cost, err, ref):
         cost = np.ascontiguousarray(cost, dtype=np.float64)

@@ -41,7 +41,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> s
            *[f"-D{d}" for d in defines], "-o", out + ".tmp"]
     if verbose:
         cmd += ["-Xptxas", "-v"]
-    cmd += [os.path.join(CSRC, s) for s in SOURCES]
+    cmd += [os.path.join(CSRC, s) for s in SOURCES] + ["-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

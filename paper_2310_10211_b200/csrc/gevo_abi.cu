@@ -4,10 +4,13 @@
 // initial weights and the growable device arena; validates plans; no C++
 // exception crosses the boundary.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <mutex>
 #include <string>
 #include <vector>
 #include "gevo.h"
@@ -62,6 +65,9 @@ struct gevo_ctx {
   double last_ms = 0.0;
   bool profile = false;
   DevBuf prof;
+  ncclComm_t comm = nullptr;   // gevo_comm_init: the population all-gather
+  int comm_rank = 0, comm_world = 1;
+  DevBuf gather;
 };
 
 static int fail(gevo_ctx* c, int code, const std::string& msg) {
@@ -198,6 +204,8 @@ int gevo_destroy(gevo_ctx* ctx) {
   ctx->params.release();
   ctx->outs.release();
   ctx->ns.release();
+  ctx->gather.release();
+  gevo_comm_destroy(ctx);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -696,6 +704,114 @@ int gevo_nsga2_select(gevo_ctx* ctx, const double* cost, const double* error, in
   if (keep < 0 || keep > n) return fail(ctx, GEVO_E_ARG, "keep out of range");
   return nsga2_common(ctx, cost, error, n, keep, chosen, rank, crowding, nullptr, nullptr,
                       nullptr);
+}
+
+
+// ---------------------------------------------------------------------------
+// Population all-gather over NCCL: NCCL is opened at run
+// time (dlopen "libnccl.so.2"), so the library loads on hosts without it and
+// only the multi-GPU entry points need it.
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+namespace {
+struct NcclApi {
+  bool tried = false, ok = false;
+  std::string why;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    api.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      api.why = std::string("cannot open libnccl.so.2: ") + dlerror();
+      return;
+    }
+    api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(h, "ncclAllGather"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.errorString = reinterpret_cast<decltype(api.errorString)>(dlsym(h, "ncclGetErrorString"));
+    api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy &&
+             api.errorString;
+    if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
+  });
+  return api;
+}
+
+int nccl_fail(gevo_ctx* c, ncclResult_t r, const char* what) {
+  return fail(c, GEVO_E_COMM, std::string(what) + ": " + nccl().errorString(r));
+}
+}  // namespace
+
+extern "C" {
+
+int gevo_comm_unique_id(void* out, size_t len) {
+  if (!out || len < sizeof(ncclUniqueId)) return GEVO_E_ARG;
+  NcclApi& api = nccl();
+  if (!api.ok) return GEVO_E_COMM;
+  ncclUniqueId id;
+  if (api.getUniqueId(&id) != ncclSuccess) return GEVO_E_COMM;
+  memcpy(out, &id, sizeof(id));
+  return GEVO_OK;
+}
+
+int gevo_comm_init(gevo_ctx* ctx, int rank, int world, const void* uid, size_t len) {
+  if (!ctx) return GEVO_E_ARG;
+  if (world < 1 || rank < 0 || rank >= world || !uid || len < sizeof(ncclUniqueId))
+    return fail(ctx, GEVO_E_ARG, "bad communicator arguments");
+  NcclApi& api = nccl();
+  if (!api.ok) return fail(ctx, GEVO_E_COMM, api.why);
+  CK(cudaSetDevice(ctx->device));
+  gevo_comm_destroy(ctx);
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof(id));
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = api.commInitRank(&comm, world, id, rank);
+  if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclCommInitRank");
+  ctx->comm = comm;
+  ctx->comm_rank = rank;
+  ctx->comm_world = world;
+  return GEVO_OK;
+}
+
+int gevo_comm_destroy(gevo_ctx* ctx) {
+  if (!ctx) return GEVO_E_ARG;
+  if (ctx->comm) {
+    nccl().commDestroy(ctx->comm);
+    ctx->comm = nullptr;
+  }
+  ctx->comm_rank = 0;
+  ctx->comm_world = 1;
+  return GEVO_OK;
+}
+
+int gevo_allgather(gevo_ctx* ctx, const void* send, size_t bytes, void* recv) {
+  if (!ctx) return GEVO_E_ARG;
+  if (!ctx->comm) return fail(ctx, GEVO_E_STATE, "gevo_comm_init has not been called");
+  if ((!send || !recv) && bytes) return fail(ctx, GEVO_E_ARG, "null buffer");
+  CK(cudaSetDevice(ctx->device));
+  const size_t total = bytes * (size_t)ctx->comm_world;
+  if (ctx->gather.ensure(bytes + total + 16, ctx->stream))
+    return fail(ctx, GEVO_E_CUDA, "gather alloc failed");
+  char* dsend = static_cast<char*>(ctx->gather.p);
+  char* drecv = dsend + ((bytes + 15) & ~size_t(15));
+  CK(cudaMemcpyAsync(dsend, send, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  ncclResult_t r = nccl().allGather(dsend, drecv, bytes, ncclUint8, ctx->comm, ctx->stream);
+  if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclAllGather");
+  CK(cudaMemcpyAsync(recv, drecv, total, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return GEVO_OK;
 }
 
 }  // extern "C"

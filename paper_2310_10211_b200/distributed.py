@@ -41,13 +41,29 @@ def pack_records(fits, records):
     return out
 
 
-def all_gather_records(local: np.ndarray, n_max: int, group=None):
-    """One all-gather (NCCL when the default group is NCCL) of per-rank
-    records padded to n_max rows; returns [world, n_max, 4] int64 and the
-    per-rank valid counts."""
+def strided_shards(n: int, world: int):
+    """Shard r = items r, r + world, r + 2*world, ... : the split used when
+    the costs are not known before the shard is lowered (patches applied in
+    the workers); deterministic, and every shard sees the same mix of
+    generations' insertion order."""
+    return [list(range(r, n, world)) for r in range(world)]
+
+
+def all_gather_records(local: np.ndarray, n_max: int, group=None, ctx=None):
+    """One all-gather of per-rank records padded to n_max rows; returns
+    [world, n_max, 4] int64 and the per-rank valid counts.  With `ctx` (a
+    libgevo Context whose NCCL communicator is initialised, see
+    init_comm) the gather is libgevo's own gevo_allgather over NVLink;
+    otherwise torch.distributed (gloo in the CPU tests)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
+    if ctx is not None:
+        buf = np.zeros((n_max + 1, RECORD_FIELDS), dtype=np.int64)
+        buf[0, 0] = len(local)
+        buf[1:len(local) + 1] = local
+        arr = ctx.allgather(buf, world)
+        return arr[:, 1:, :], arr[:, 0, 0].astype(int)
     dev = torch.device("cuda", torch.cuda.current_device()) \
         if dist.get_backend(group) == "nccl" else torch.device("cpu")
     buf = np.zeros((n_max + 1, RECORD_FIELDS), dtype=np.int64)
@@ -92,6 +108,11 @@ class ShardedEvaluator:
         self.backend = backend
         self.group = group
         self.last_shards = None
+        self.ctx = init_comm(backend, group)
+
+    @property
+    def workload(self):
+        return self.backend.workload
 
     def _world(self):
         import torch.distributed as dist
@@ -99,9 +120,31 @@ class ShardedEvaluator:
             return dist.get_world_size(self.group), dist.get_rank(self.group)
         return 1, 0
 
+    def _gather(self, fits, recs, shards, rank):
+        local = pack_records(fits, recs)
+        for k, f in enumerate(fits):
+            if not f.valid:
+                local[k, 3] = STATUS_INVALID
+        n_max = max(len(s) for s in shards)
+        gathered, counts = all_gather_records(local, n_max, self.group, self.ctx)
+        return unpack_records(merge_shards(gathered, counts, shards))
+
+    def evaluate_patches(self, original, keys, functions, holdout=False):
+        """Every rank passes the SAME patch keys (the replicated GA); rank r
+        applies, lowers and evaluates the strided shard r (in its own worker
+        processes, on its own device), then one all-gather."""
+        world, rank = self._world()
+        if world == 1:
+            return self.backend.evaluate_patches(original, keys, functions, holdout=holdout)
+        shards = strided_shards(len(keys), world)
+        self.last_shards = shards
+        fits, recs = self.backend.evaluate_patches(original, [keys[i] for i in shards[rank]],
+                                                   functions, holdout=holdout,
+                                                   return_records=True)
+        return self._gather(fits, recs, shards, rank)
+
     def evaluate_variants(self, variants, holdout=False, cost_table=None):
         from .lowering import static_cost
-        from .workloads import INVALID_FITNESS, Fitness
         world, rank = self._world()
         if world == 1:
             return self.backend.evaluate_variants(variants, holdout=holdout)
@@ -118,21 +161,42 @@ class ShardedEvaluator:
         mine = [variants[i] for i in shards[rank]]
         fits, recs = self.backend.evaluate_variants(mine, holdout=holdout,
                                                     return_records=True)
-        local = pack_records(fits, recs)
-        for k, f in enumerate(fits):
-            if not f.valid:
-                local[k, 3] = STATUS_INVALID
-        n_max = max(len(s) for s in shards)
-        gathered, counts = all_gather_records(local, n_max, self.group)
-        merged = merge_shards(gathered, counts, shards)
-        out = []
-        for row in merged:
-            cost = float(np.int64(row[0]).view(np.float64))
-            status = int(row[3])
-            if status == STATUS_INVALID:
-                out.append(INVALID_FITNESS)
-            elif status != 0:
-                out.append(Fitness(cost, 1.0))
-            else:
-                out.append(Fitness(cost, int(row[1]) / int(row[2])))
-        return out
+        return self._gather(fits, recs, shards, rank)
+
+
+def unpack_records(merged):
+    """Gathered int64 records -> Fitness list, with the reference's
+    encodings (fitness.py:376-392) and error = wrong / total in Python."""
+    from .workloads import INVALID_FITNESS, Fitness
+    out = []
+    for row in merged:
+        cost = float(np.int64(row[0]).view(np.float64))
+        status = int(row[3])
+        if status == STATUS_INVALID:
+            out.append(INVALID_FITNESS)
+        elif status != 0:
+            out.append(Fitness(cost, 1.0))
+        else:
+            out.append(Fitness(cost, int(row[1]) / int(row[2])))
+    return out
+
+
+def init_comm(backend, group=None):
+    """When the process group is NCCL and `backend` owns a libgevo context,
+    create libgevo's own NCCL communicator over the same ranks (rank 0's
+    ncclUniqueId is broadcast through the process group: torch.distributed
+    is the plumbing, the records travel through gevo_allgather).  Returns
+    the context, or None (gloo / single rank: torch's all-gather)."""
+    import torch.distributed as dist
+    ctx = getattr(backend, "ctx", None)
+    if ctx is None or not (dist.is_available() and dist.is_initialized()):
+        return None
+    if dist.get_backend(group) != "nccl" or dist.get_world_size(group) == 1:
+        return None
+    from . import _lib
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    box = [_lib.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0,
+                               group=group)
+    ctx.comm_init(rank, world, box[0])
+    return ctx

@@ -19,8 +19,8 @@ import time
 import numpy as np
 
 from . import _lib
-from .plan import (build_population_plan, device_weight, layout_order, lower_variant,
-                   sm_aware_order)
+from .plan import (UnsupportedVariant, build_population_plan, device_weight, layout_order,
+                   lower_variant, sm_aware_order)
 from .workloads import (INVALID_FITNESS, PREDICTION, TRAINING, WEIGHT_NAMES,
                         Fitness, Workload)
 
@@ -28,15 +28,34 @@ SPLIT_SEARCH, SPLIT_HOLDOUT = 0, 1
 STATUS_OK, STATUS_NONFINITE_WEIGHTS, STATUS_NONFINITE_PROBS = 0, 1, 2
 POOL_MIN = 32          # variants below which lowering stays in-process
 _POOL = None
+# original modules the workers apply patches to (evaluate_patches): a
+# worker inherits this table when it is forked, so a module registered after
+# the pool was created re-forks the pool once
+_MODULES: dict = {}
+_POOL_TOKENS: frozenset = frozenset()
 
 
-def _lower_pool():
-    """Process pool for host lowering (pure Python/numpy, GIL-bound): one
-    worker per core, created once.  Workers are forked (no re-import of
-    __main__) and only run lowering -- they never touch CUDA.
+def register_module(module) -> str:
+    """Make `module` (an evotir Module: the workload's original program)
+    available to the lowering workers; returns its token."""
+    tok = f"m{id(module):x}"
+    if _MODULES.get(tok) is not module:
+        _MODULES[tok] = module
+    return tok
+
+
+def _lower_pool(token=None):
+    """Process pool for host work (pure Python/numpy, GIL-bound): one worker
+    per core, created once (re-forked when `token` names a module the
+    workers have not inherited).  Workers are forked (no re-import of
+    __main__) and only apply patches and lower -- they never touch CUDA.
     GEVO_B200_LOWER_WORKERS=1 disables it."""
-    global _POOL
+    global _POOL, _POOL_TOKENS
+    if _POOL and token is not None and token not in _POOL_TOKENS:
+        _POOL.shutdown(wait=False, cancel_futures=True)
+        _POOL = None
     if _POOL is None:
+        _POOL_TOKENS = frozenset(_MODULES)
         # one share of the host's cores per local rank (torchrun sets
         # LOCAL_WORLD_SIZE; every rank of a node lowers its own shard)
         share = (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
@@ -55,29 +74,67 @@ def _lower_pool():
 
 def _lower_many(batch):
     """Worker: lower a list of variants; None for a variant that fails
-    (evaluate() maps any exception to INVALID_FITNESS)."""
+    (evaluate() maps any exception to INVALID_FITNESS), the exception itself
+    for a valid variant the device cannot run (raised by the caller)."""
     fns_list, cost_table, training, steps = batch
     out = []
     for fns in fns_list:
         try:
             out.append(lower_variant(fns, cost_table, training=training, steps=steps))
+        except UnsupportedVariant as e:
+            out.append(e)
         except Exception:
             out.append(None)
     return out
 
 
-def _submit_lowering(variants, idx, cost_table, training, steps=600):
-    """Start lowering variants[idx] (None entries excluded by the caller).
-    Returns a list of (positions, future-or-result) in idx order."""
-    pool = _lower_pool() if len(idx) >= POOL_MIN else None
+def _lower_patches(batch):
+    """Worker: the body of the reference's evaluate() up to execution, for a
+    list of patches (canonical patch JSON, genome.py:302-309): apply_patch +
+    verify (genome.py:482-516) -- a PatchApplicationError is the reference's
+    INVALID_FITNESS (fitness.py:375-377), None here -- then lowering."""
+    token, keys, functions, cost_table, training, steps = batch
+    from evotir.genome import PatchApplicationError, apply_patch, patch_loads
+    original = _MODULES[token]
+    out = []
+    for key in keys:
+        try:
+            m = apply_patch(original, patch_loads(key)).module
+        except PatchApplicationError:
+            out.append(None)
+            continue
+        out.extend(_lower_many(([{n: m.functions[n] for n in functions}],
+                                cost_table, training, steps)))
+    return out
+
+
+def _check_supported(vp):
+    if isinstance(vp, UnsupportedVariant):
+        raise _lib.GevoError(str(vp))
+    return vp
+
+
+def _submit_lowering(variants, idx, cost_table, training, steps=600, patches=None):
+    """Start lowering variants[idx] (None entries excluded by the caller), or
+    -- with patches=(token, keys, functions) -- applying and lowering
+    keys[idx] in the workers.  Returns a list of (positions, future-or-result)
+    in idx order."""
+    if patches is not None:
+        token, keys, functions = patches
+        fn = _lower_patches
+        args = lambda c: (token, [keys[i] for i in c], functions, cost_table, training, steps)
+    else:
+        fn = _lower_many
+        args = lambda c: ([variants[i] for i in c], cost_table, training, steps)
+    pool = _lower_pool(patches[0] if patches else None) if len(idx) >= POOL_MIN else None
     if pool is None:
-        return [(list(idx), _lower_many(([variants[i] for i in idx], cost_table, training, steps)))]
+        return [(list(idx), fn(args(idx)))]
     nw = pool._max_workers
     per = max(4, (len(idx) + 2 * nw - 1) // (2 * nw))
     out = []
     for k in range(0, len(idx), per):
         c = idx[k:k + per]
-        out.append((c, pool.submit(_lower_many, ([variants[i] for i in c], cost_table, training, steps))))
+        out.append((c, pool.submit(fn, args(c))))
     return out
 
 
@@ -95,7 +152,7 @@ def lower_all(variants, cost_table, training, steps=600):
     idx = [i for i, v in enumerate(variants) if v is not None]
     out = [None] * len(variants)
     for i, r in zip(*_collect(_submit_lowering(variants, idx, cost_table, training, steps))):
-        out[i] = r
+        out[i] = _check_supported(r)
     return out
 
 
@@ -179,7 +236,9 @@ class DeviceEvaluator:
     def _ensure_holdout(self):
         if self._holdout_batches is None:
             ds, cfg = self.workload.dataset, self.workload.config
-            ds.holdout.reads += 1      # the only reader of holdout (fitness.py:404)
+            # holdout.reads is bumped by the holdout_report seam, once per
+            # report like the reference (fitness.py:407); the upload is not a
+            # report
             for c in (self.ctx, self._ctx2):
                 if c is not None:
                     upload_split(c, SPLIT_HOLDOUT, ds.holdout, cfg.classes, cfg.batch_size)
@@ -187,8 +246,18 @@ class DeviceEvaluator:
         return self._holdout_batches
 
     # ------------------------------------------------------------------
+    def evaluate_patches(self, original, keys, functions, holdout=False,
+                         return_records=False):
+        """The reference's evaluate() (fitness.py:372-393) for a list of
+        patches given as canonical patch JSON (genome.patch_dumps, the
+        _Evaluator cache keys): apply_patch, verification and lowering run in
+        the worker processes, so the parent only packs and launches."""
+        return self.evaluate_variants(keys, holdout=holdout, return_records=return_records,
+                                      _patches=(register_module(original), list(keys),
+                                                list(functions)))
+
     def evaluate_variants(self, variants, holdout=False, want_weights=False,
-                          return_records=False):
+                          return_records=False, _patches=None):
         """variants: list of {'train_step': fn, 'forward': fn} (or None for
         a patch that failed to apply).  Returns list[Fitness] (and the raw
         device records when return_records)."""
@@ -213,12 +282,13 @@ class DeviceEvaluator:
         # two halves when the pool is used: half A runs on the device (ctypes
         # releases the GIL) while half B is still being lowered
         halves = [idx]
-        if len(idx) >= 2 * POOL_MIN and _lower_pool() is not None and \
-                os.environ.get("GEVO_B200_HALVES", "1") != "0":
+        if len(idx) >= 2 * POOL_MIN and _lower_pool(_patches[0] if _patches else None) is not None \
+                and os.environ.get("GEVO_B200_HALVES", "1") != "0":
             halves = [idx[:len(idx) // 2], idx[len(idx) // 2:]]
-        jobs = [_submit_lowering(variants, h, cfg.cost_table, training, cfg.steps) for h in halves]
+        jobs = [_submit_lowering(variants, h, cfg.cost_table, training, cfg.steps, _patches)
+                for h in halves]
         ctxs = [self.ctx, self._second_context() if len(halves) > 1 else None]
-        runner, box, launches = None, {}, {}
+        runner, box, launches, failed = None, {}, {}, {}
         t_lower = t_pack = 0.0
         plan_bytes = 0
         for h, job in enumerate(jobs):
@@ -227,6 +297,7 @@ class DeviceEvaluator:
             tb = time.perf_counter()
             lowered, slots = [], []
             for i, vp in zip(pos, vps):
+                vp = _check_supported(vp)
                 if vp is None:
                     fits[i] = INVALID_FITNESS  # evaluate(): any exception
                 else:
@@ -260,17 +331,20 @@ class DeviceEvaluator:
                          cfg.finite_check_every, SPLIT_SEARCH, split, self.weight_elems, want_weights)
 
             def run(c=ctxs[h], pl=plans, ma=mode_args, key=h, lv=lowered, sl=slots):
-                recs, fws, od, ms = [], [], None, 0.0
-                for plan, order_, n_g in pl:
-                    res, fw = c.eval(plan.blob, plan.n_prog, *ma)
-                    ms += c.last_kernel_ms()
-                    recs.append(res[:n_g])
-                    fws.append(fw[:n_g] if fw is not None else None)
-                    od = order_
-                res = np.concatenate(recs)
-                fw = np.concatenate(fws) if fws and fws[0] is not None else None
-                box[key] = ((res, fw), lv, sl, od)
-                launches[key] = (len(pl), ms)
+                try:
+                    recs, fws, od, ms = [], [], None, 0.0
+                    for plan, order_, n_g in pl:
+                        res, fw = c.eval(plan.blob, plan.n_prog, *ma)
+                        ms += c.last_kernel_ms()
+                        recs.append(res[:n_g])
+                        fws.append(fw[:n_g] if fw is not None else None)
+                        od = order_
+                    res = np.concatenate(recs)
+                    fw = np.concatenate(fws) if fws and fws[0] is not None else None
+                    box[key] = ((res, fw), lv, sl, od)
+                    launches[key] = (len(pl), ms)
+                except BaseException as e:   # re-raised by the caller after join
+                    failed[key] = e
             if h + 1 < len(jobs):
                 import threading
                 runner = threading.Thread(target=run)
@@ -279,6 +353,9 @@ class DeviceEvaluator:
                 run()
         if runner is not None:
             runner.join()
+        if failed:
+            # a device failure in either half is loud, never a missing fitness
+            raise failed[min(failed)]
         used = sorted(box)
         if any(launches[k][0] > 1 for k in used):
             # consecutive launches (scratch budget): kernel time summed per
@@ -305,6 +382,9 @@ class DeviceEvaluator:
                     fits[i] = Fitness(cost, wrong[k] / total[k])
                 if want_weights:
                     finals[i] = fw[k]
+        missing = [i for i, f in enumerate(fits) if f is None]
+        if missing:
+            raise _lib.GevoError(f"no fitness for variants {missing[:8]} (internal error)")
         self.last_plan_bytes = plan_bytes
         self.last_timing = {"lower_wait_s": t_lower, "pack_s": t_pack,
                             "total_s": time.perf_counter() - t0, "n": len(idx),
@@ -384,13 +464,16 @@ def baseline_functions(workload: Workload) -> dict:
 def train_baseline_weights(workload: Workload, device: int = 0) -> dict:
     """Weights after training the unmutated program (fitness.py:265-270),
     on the device."""
+    from .workloads import WorkloadError
     ev = DeviceEvaluator(workload, device)
     try:
-        (fit,), _, (flat,) = ev.evaluate_variants(
+        (fit,), recs, (flat,) = ev.evaluate_variants(
             [baseline_functions(workload)], want_weights=True,
             return_records=True)
-        if fit.error == 1.0 and flat is None:
-            raise RuntimeError("baseline training diverged; cannot freeze")
+        # the reference refuses to freeze weights that went non-finite at a
+        # check step or at the end (fitness.py:266-269)
+        if int(recs[0]["status"]) != STATUS_OK or not fit.valid:
+            raise WorkloadError("baseline training diverged; cannot freeze")
         return ev.split_weights(flat)
     finally:
         ev.close()

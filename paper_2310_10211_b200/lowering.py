@@ -77,7 +77,6 @@ HEADER_DTYPE = np.dtype([
 assert INSTR_DTYPE.itemsize == 224 and PROG_DTYPE.itemsize == 112
 assert HEADER_DTYPE.itemsize == 80
 
-FLAG_LAYOUT_APPROX = 1     # returned layouts have no period <= 2 (gevo_plan.h)
 FLAG_ALTERNATE = 2         # layouts alternate: steps >= 1 odd -> train1, even -> train0
 
 _NP_DTYPE = {K_F64: np.float64, K_I64: np.int64, K_I1: np.int64}

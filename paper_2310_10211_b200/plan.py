@@ -12,10 +12,16 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import layout as L
-from .lowering import (BUF_OUT0, FLAG_ALTERNATE, FLAG_LAYOUT_APPROX, HEADER_DTYPE,
+from .lowering import (BUF_OUT0, FLAG_ALTERNATE, HEADER_DTYPE,
                        INSTR_DTYPE, PLAN_MAGIC, PLAN_VERSION, PROG_DTYPE,
                        consts_to_words, encode_instrs, lower_function,
                        static_cost)
+
+
+class UnsupportedVariant(Exception):
+    """A valid variant this executor cannot run bit-exactly.  Never mapped to
+    a fitness: the evaluator raises it as a GevoError (no silent
+    approximation, no fallback)."""
 
 
 @dataclass
@@ -78,12 +84,14 @@ def lower_variant(functions: dict, cost_table=None, training=True,
                 flags |= FLAG_ALTERNATE
                 final = L0 if (steps - 1) % 2 == 0 else L1
             else:
-                # no period <= 2 (never seen): later steps approximated by
-                # the layout after step 1, and the individual flagged
-                layouts[:nw] = L1
-                low1 = lower_function(ts, layouts, cost_table=cost_table)
-                flags |= FLAG_LAYOUT_APPROX
-                final = list(low1.ret_strides)
+                # the weights' numpy layouts do not settle within two steps
+                # (C -> L0 -> L1 with L1 not in {C, L0}); never seen in any
+                # recorded population.  The summation orders of later steps
+                # depend on those layouts, so refuse loudly rather than run
+                # step >= 2 with the wrong program.
+                raise UnsupportedVariant(
+                    "train_step returns weight layouts with no period <= 2 "
+                    f"(step 0 -> {L0}, step 1 -> {L1}); not supported by the device executor")
         t0 = _encode_shifted(low0, consts)
         t1 = t0 if low1 is low0 else _encode_shifted(low1, consts)
         arena = max(low0.arena_elems, low1.arena_elems)

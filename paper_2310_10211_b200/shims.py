@@ -91,6 +91,25 @@ def device_for(workload, device: int = 0):
     return ev
 
 
+_SHARDED: dict = {}
+
+
+def sharded_for(workload, device: int = 0):
+    """The population-sharded evaluator (distributed.ShardedEvaluator over
+    this rank's DeviceEvaluator) when torch.distributed is initialised with
+    more than one rank; the plain device evaluator otherwise."""
+    from . import distributed as D
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
+        return device_for(workload, device)
+    key = (id(workload), device)
+    ev = _SHARDED.get(key)
+    if ev is None or ev.backend.workload.source is not workload:
+        ev = D.ShardedEvaluator(device_for(workload, device))
+        _SHARDED[key] = ev
+    return ev
+
+
 def _variants(original, patches, functions):
     """apply_patch each patch (genome.py:482-516); None when it fails."""
     _, G, _ = _E()
@@ -119,7 +138,14 @@ class GpuEvaluator:
     """Same interface as evotir.search._Evaluator: `.workload`, `.cache`
     (patch_dumps key -> Fitness, insertion ordered), `.threads`; a call
     evaluates every fresh patch of the list in ONE device launch and returns
-    the fitness of every requested patch in request order."""
+    the fitness of every requested patch in request order.
+
+    The fresh patches travel as their cache keys (canonical patch JSON):
+    apply_patch + verify (genome.py:482-516) and the lowering run in the
+    evaluator's worker processes, not serially here.  Under torch.distributed
+    with several ranks (install() on every rank), each rank evaluates a
+    shard of the fresh patches on its own GPU and one all-gather
+    (gevo_allgather, NCCL) hands every rank every fitness."""
 
     def __init__(self, workload, device: int = 0, backend=None):
         self.workload = workload
@@ -131,7 +157,7 @@ class GpuEvaluator:
     @property
     def backend(self):
         if self._backend is None:
-            self._backend = device_for(self.workload, self.device)
+            self._backend = sharded_for(self.workload, self.device)
         return self._backend
 
     def __call__(self, patches):
@@ -143,10 +169,15 @@ class GpuEvaluator:
                 fresh[key] = p
         if fresh:
             items = list(fresh.items())
-            variants = _variants(self.workload.module, [p for _, p in items],
-                                 _functions(self.workload))
-            fits = _to_ref(self.backend.evaluate_variants(variants))
-            for (key, _), fit in zip(items, fits):
+            be = self.backend
+            if hasattr(be, "evaluate_patches"):
+                fits = be.evaluate_patches(self.workload.module, [k for k, _ in items],
+                                           _functions(self.workload))
+            else:                   # test backends that take applied variants
+                fits = be.evaluate_variants(_variants(self.workload.module,
+                                                      [p for _, p in items],
+                                                      _functions(self.workload)))
+            for (key, _), fit in zip(items, _to_ref(fits)):
                 self.cache[key] = fit
         return [self.cache[key] for key, _ in keyed]
 
@@ -187,12 +218,15 @@ def holdout_report(original, patch, w, backend=None):
 # ---------------------------------------------------------------------------
 
 _NS_CTX = None
+_NS_DEVICE = 0          # set by install(device=...)
 
 
 def _ns_ctx():
+    """The context NSGA-II, archive and hypervolume run on: the device
+    install() was given (each rank of a multi-GPU run uses its own)."""
     global _NS_CTX
-    if _NS_CTX is None:
-        _NS_CTX = _lib.Context(0)
+    if _NS_CTX is None or _NS_CTX.device != _NS_DEVICE:
+        _NS_CTX = _lib.Context(_NS_DEVICE)
     return _NS_CTX
 
 
@@ -242,7 +276,9 @@ def select_survivors(pool, n):
     if not pool:
         return []
     c, e = _arrays([ind.fitness.as_tuple() for ind in pool])
-    chosen, rank, crowd = _ns_ctx().nsga2_select(c, e, n)
+    # asking for more than the pool takes every front whole (the reference's
+    # loop simply runs out of fronts)
+    chosen, rank, crowd = _ns_ctx().nsga2_select(c, e, max(0, min(int(n), len(pool))))
     last = int(rank[chosen].max()) if len(chosen) else 0
     for i, ind in enumerate(pool):
         if rank[i] <= last:
@@ -364,10 +400,19 @@ class Archive:
 _SAVED: dict = {}
 
 
-def install(device: int = 0, nsga2: bool = True):
-    """Rebind the reference's evaluation seams to the device versions."""
+def install(device: int | None = None, nsga2: bool = True, backend_factory=None):
+    """Rebind the reference's evaluation seams to the device versions.
+    `device` defaults to LOCAL_RANK (0 outside torchrun); with
+    torch.distributed initialised over several ranks the evaluator shards
+    each generation's fresh patches over the ranks (one GPU each).
+    `backend_factory(workload)` substitutes the evaluator backend (tests)."""
+    import os
     import evotir.cli as C
+    global _NS_DEVICE
     _, _, S = _E()
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", "0"))
+    _NS_DEVICE = device
     if not _SAVED:
         _SAVED.update({
             ("search", "_Evaluator"): S._Evaluator,
@@ -385,7 +430,8 @@ def install(device: int = 0, nsga2: bool = True):
 
     class _Bound(GpuEvaluator):
         def __init__(self, workload):
-            super().__init__(workload, device)
+            super().__init__(workload, device,
+                             backend=backend_factory(workload) if backend_factory else None)
 
     S._Evaluator = _Bound
     S.evaluate = C.evaluate = evaluate

@@ -16,10 +16,18 @@ reference's own interpreter and mutation engine run on the network text:
     (fitness.py:355-369), and its static cost is the reference's
     (interpreter.py:41-59, fitness.py:387-388).
 
-Writes tests/golden/cnn_pop.json.gz.
+Writes tests/golden/cnn_pop.json.gz (the reduced 4-block net, 30 images).
+
+    ... make_cnn_golden.py full
+
+records the BASELINE.json configs[2] network itself (MobileNetV2-CIFAR width
+0.5, cnn.MOBILENETV2_CIFAR_HALF, batch 100) over 100 images with 16
+reference-made mutants (about 10 min on one core) into
+tests/golden/cnn_full_pop.json.gz.
 """
 from __future__ import annotations
 
+import base64
 import gzip
 import json
 import os
@@ -48,8 +56,12 @@ def fn_text(fn) -> str:
     return print_module(Module(functions={fn.name: fn}, constants={}))
 
 
-def main():
-    cfg = cnn.CnnConfig(search_n=30, holdout_n=10)
+def main(full=False):
+    if full:
+        cfg = cnn.CnnConfig(**cnn.MOBILENETV2_CIFAR_HALF, batch_size=100, search_n=100,
+                            holdout_n=100)
+    else:
+        cfg = cnn.CnnConfig(search_n=30, holdout_n=10)
     wl = cnn.build_cnn_prediction_workload(cfg)
     text, flat = cnn.cnn_forward_text(cfg)
     module = parse_module(text)
@@ -101,17 +113,25 @@ def main():
         rec = score(mod)
         rec.update(key=patch_dumps(patch), edits=len(patch),
                    forward=fn_text(mod.functions["forward"]))
+        if full:
+            # the probabilities of batch 0 as the reference computes them:
+            # a bit-level check far stronger than the error of a frozen
+            # random-init network (near chance for every variant)
+            p0 = np.ascontiguousarray(probs_of(mod, xs[0]), dtype=np.float64)
+            rec["probs0_b64"] = base64.b64encode(p0.tobytes()).decode()
         inds.append(rec)
         print(f"edits {len(patch)}: cost {rec['cost']:.0f} wrong {rec['wrong']}/{rec['total']} "
               f"status {rec['status']}")
     out = {"config": {"search_n": cfg.search_n, "holdout_n": cfg.holdout_n,
                       "batch_size": cfg.batch_size},
            "individuals": inds}
-    path = os.path.join(HERE, "cnn_pop.json.gz")
+    if full:
+        out["config"]["network"] = "MOBILENETV2_CIFAR_HALF"
+    path = os.path.join(HERE, "cnn_full_pop.json.gz" if full else "cnn_pop.json.gz")
     with gzip.open(path, "wt") as f:
         json.dump(out, f, separators=(",", ":"), sort_keys=True)
     print(f"wrote {path} ({os.path.getsize(path)} bytes)")
 
 
 if __name__ == "__main__":
-    main()
+    main(full=sys.argv[1:2] == ["full"])

@@ -35,19 +35,25 @@ def predict_weights():
     return {n: arc[n] for n in ("w1", "b1", "w2", "b2")}
 
 
+REF_DIRS = ("/root/reference/pkg/src",          # the build container
+            os.path.join(os.path.dirname(GOLDEN), "..", "baseline", "_ref"))  # baseline/install_ref.sh
+
+
 def reference_available():
+    """Import the unmodified reference: from /root/reference here, or from
+    the baseline/_ref install that travels to the GPU box."""
     try:
         import evotir  # noqa: F401
         return True
     except ImportError:
-        ref = "/root/reference/pkg/src"
-        if os.path.isdir(ref):
-            sys_path_add(ref)
-            try:
-                import evotir  # noqa: F401
-                return True
-            except ImportError:
-                return False
+        for ref in REF_DIRS:
+            if os.path.isdir(os.path.join(ref, "evotir")):
+                sys_path_add(os.path.abspath(ref))
+                try:
+                    import evotir  # noqa: F401
+                    return True
+                except ImportError:
+                    continue
         return False
 
 

@@ -46,3 +46,43 @@ def test_plan_struct_sizes_match_header():
     hdr = open(os.path.join(ROOT, "include", "gevo_plan.h")).read()
     assert "/* 224 bytes */" in hdr and "/* 112 bytes */" in hdr
     assert Lw.INSTR_DTYPE.itemsize == 224 and Lw.PROG_DTYPE.itemsize == 112
+
+
+def _c_sizeof(types):
+    """sizeof of header types, from a C probe compiled against include/."""
+    import subprocess
+    import tempfile
+    src = "#include <stdio.h>\n#include \"gevo.h\"\nint main(void){" + "".join(
+        f'printf("%zu\\n", sizeof({t}));' for t in types) + "return 0;}\n"
+    with tempfile.TemporaryDirectory() as d:
+        c, exe = os.path.join(d, "p.c"), os.path.join(d, "p")
+        open(c, "w").write(src)
+        subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe], check=True)
+        out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout
+    return [int(x) for x in out.split()]
+
+
+def test_result_and_plan_sizes_match_c_header():
+    from paper_2310_10211_b200 import lowering as Lw
+    res, desc, instr, prog, hdr = _c_sizeof(["gevo_result", "gevo_eval_desc", "gevo_instr",
+                                             "gevo_prog", "gevo_plan_header"])
+    assert res == _lib.RESULT_DTYPE.itemsize == 56
+    assert desc == ctypes.sizeof(_lib.GevoEvalDesc)
+    assert (instr, prog, hdr) == (Lw.INSTR_DTYPE.itemsize, Lw.PROG_DTYPE.itemsize,
+                                  Lw.HEADER_DTYPE.itemsize)
+
+
+def test_integration_stub_matches_header():
+    """The ctypes stub INTEGRATION.md tells a maintainer to add: executed up
+    to its declarations against the built library; its gevo_result must be
+    the header's 56 bytes (a shorter struct would overflow `res`)."""
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    block = text.split("```python\n# evotir/_gevo.py")[1].split("```")[0]
+    decl = block.split("ctx = ctypes.c_void_p()")[0]
+    decl = decl.replace('ctypes.CDLL("libgevo.so")', f"ctypes.CDLL({build.build()!r})")
+    ns = {}
+    exec("import ctypes, numpy as np\n#" + decl, ns)
+    (res,) = _c_sizeof(["gevo_result"])
+    assert ctypes.sizeof(ns["gevo_result"]) == res
+    assert ctypes.sizeof(ns["gevo_eval_desc"]) == ctypes.sizeof(_lib.GevoEvalDesc)
+    assert [f for f, _ in ns["gevo_result"]._fields_] == list(_lib.RESULT_DTYPE.names)

@@ -67,3 +67,72 @@ def test_device_matches_reference_on_mutants(wl, golden):
         exact += (int(r["wrong"]), int(r["total"])) == (ind["wrong"], ind["total"])
         assert f.error == ind["error"], (ind["edits"], f, ind)
     print(f"cnn mutants bit-exact {exact}/{len(fits)}")
+
+
+# --------------------------------------------------------------------------
+# configs[2] at full network size (MobileNetV2-CIFAR width 0.5, batch 100):
+# 16 reference-made mutants over 100 images (tests/golden/cnn_full_pop.json.gz,
+# make_cnn_golden.py full), with the reference's batch-0 probabilities
+
+@pytest.fixture(scope="module")
+def full_golden():
+    return load("cnn_full_pop.json.gz")
+
+
+@pytest.fixture(scope="module")
+def full_wl(full_golden):
+    c = full_golden["config"]
+    assert c["network"] == "MOBILENETV2_CIFAR_HALF"
+    return cnn.build_cnn_prediction_workload(
+        cnn.CnnConfig(**cnn.MOBILENETV2_CIFAR_HALF, search_n=c["search_n"],
+                      holdout_n=c["holdout_n"], batch_size=c["batch_size"]))
+
+
+def _probs0(ind):
+    import base64
+    return np.frombuffer(base64.b64decode(ind["probs0_b64"]), dtype=np.float64).reshape(100, 10)
+
+
+def test_full_network_mutants_cost_and_oracle(full_wl, full_golden):
+    """Static cost of all 16 full-size variants, and the oracle's batch-0
+    probabilities for the unmutated network and one mutant, bit-exact."""
+    from oracle import interp as OI
+    inds = full_golden["individuals"]
+    assert len(inds) >= 16 and sum(i["edits"] > 0 for i in inds) >= 15
+    xb = full_wl.search_x.reshape(-1, 100, 32, 32, 3)[0]
+    for k, ind in enumerate(inds):
+        fn = dialect.parse_function(ind["forward"])
+        assert static_cost(fn) * 1 == ind["cost"]
+        if k in (0, 1):
+            (p,) = OI.Program(fn)([full_wl.weights["w"], xb])
+            assert np.array_equal(p, _probs0(ind))
+
+
+@pytest.mark.gpu
+def test_device_full_network_mutants(full_wl, full_golden):
+    """Every full-size mutant on the device: (cost, wrong, total, status)
+    through the evaluator and the batch-0 probabilities through
+    gevo_exec_once, bit-exact against the reference."""
+    from paper_2310_10211_b200 import _lib
+    from paper_2310_10211_b200.evaluator import DeviceEvaluator
+    from test_gpu_parity import run_once
+    inds = full_golden["individuals"]
+    fns = [dialect.parse_function(i["forward"]) for i in inds]
+    ev = DeviceEvaluator(full_wl)
+    fits, recs = ev.evaluate_variants([{"forward": f} for f in fns], return_records=True)
+    ev.close()
+    for ind, f, r in zip(inds, fits, recs):
+        assert f.cost == ind["cost"]
+        assert (int(r["status"]), int(r["wrong"]), int(r["total"])) == \
+            (ind["status"], ind["wrong"], ind["total"]), ind["edits"]
+        assert f.error == ind["error"]
+    xb = np.ascontiguousarray(full_wl.search_x.reshape(-1, 100, 32 * 32 * 3)[0]).reshape(-1)
+    ctx = _lib.Context(0)
+    try:
+        outs = run_once(ctx, fns, [[full_wl.weights["w"], xb]] * len(fns))
+    finally:
+        ctx.close()
+    exact = sum(np.array_equal(got, _probs0(ind)) for (got,), ind in zip(outs, inds))
+    print(f"full-size cnn mutants: records {len(inds)}/{len(inds)}, batch-0 probabilities "
+          f"bit-exact {exact}/{len(inds)}")
+    assert exact == len(inds)

@@ -105,3 +105,93 @@ def test_two_rank_gather_matches_single_rank():
         assert fits == want                       # every rank holds every fitness
         assert seen == sizes[rank]                # and evaluated only its shard
     assert sum(out[0][3]) == len(want)
+
+
+class PatchTable:
+    """Device stand-in with the patch interface (evaluate_patches): applies
+    each patch with the reference's apply_patch and answers the reference's
+    recorded fitness for the resulting program text."""
+
+    def __init__(self, workload):
+        self.workload = workload
+        self.inner = TableBackend()
+        self.keys = []
+
+    def evaluate_patches(self, original, keys, functions, holdout=False, return_records=False):
+        from evotir.genome import PatchApplicationError, apply_patch, patch_loads
+        self.keys.extend(keys)
+        variants = []
+        for k in keys:
+            try:
+                m = apply_patch(original, patch_loads(k)).module
+            except PatchApplicationError:
+                variants.append(None)
+                continue
+            variants.append({n: m.functions[n] for n in functions})
+        return self.inner.evaluate_variants(variants, return_records=return_records)
+
+
+def _search_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from golden_io import reference_available
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        assert reference_available()
+        import evotir.search as S
+        from evotir import fitness as F
+        from paper_2310_10211_b200 import shims
+        data = load("train_pop.json.gz")
+        tables = []
+
+        def factory(w):
+            t = PatchTable(w)
+            tables.append(t)
+            return D.ShardedEvaluator(t)
+        ref_holdout = S.holdout_report
+        shims.install(nsga2=False, backend_factory=factory)
+        S.holdout_report = ref_holdout     # the archive's holdout reports stay on the host here
+        try:
+            res = S.run_search(F.build_2fcnet_workload(), S.SearchConfig(**data["config"]))
+        finally:
+            shims.uninstall()
+        keys = ("generation", "evaluations", "front_size", "best_error", "best_cost",
+                "archive_size", "hypervolume", "archive_hypervolume")
+        q.put((rank, [{k: h[k] for k in keys} for h in res.history], res.evaluations,
+               len(tables[0].keys)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not __import__("golden_io").reference_available(),
+                    reason="reference package not importable")
+def test_two_rank_run_search_under_install_reproduces_history():
+    """configs[1]'s shape in miniature: the reference's run_search on two
+    ranks with shims.install(), each generation's fresh patches sharded over
+    the ranks and all-gathered -- the recorded history comes out on both."""
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_search_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    try:
+        out = sorted(q.get(timeout=300) for _ in procs)
+    finally:
+        for p in procs:
+            p.join(60)
+            if p.is_alive():
+                p.kill()
+    for p in procs:
+        assert p.exitcode == 0
+    data = load("train_pop.json.gz")
+    keys = ("generation", "evaluations", "front_size", "best_error", "best_cost",
+            "archive_size", "hypervolume", "archive_hypervolume")
+    want = [{k: h[k] for k in keys} for h in data["history"]]
+    for rank, hist, evals, n_local in out:
+        assert hist == want
+        assert evals == len(data["individuals"])
+    # each rank evaluated only its strided shard of every call
+    assert out[0][3] + out[1][3] == len(data["individuals"])
+    assert 0 < out[1][3] <= out[0][3]

@@ -188,15 +188,15 @@ def test_reduce_order_matches_numpy():
 def test_returned_layout_cycles_are_exact():
     """Steps >= 1 read the layout the previous step stored.  A program whose
     stored layout flips every step (a returned pad of a transposed slice:
-    C -> F -> C ...) runs train0/train1 alternately (FLAG_ALTERNATE); no
-    recorded individual needs the approximate fallback."""
+    C -> F -> C ...) runs train0/train1 alternately (FLAG_ALTERNATE); a
+    longer cycle is refused (plan.UnsupportedVariant), and no recorded
+    individual has one."""
     from golden_io import load as gl
     inds = gl("bench_train_pool.json.gz")["individuals"]
     flags = []
     for ind in inds:
         vp = lower_variant({k: dialect.parse_function(ind[k]) for k in ("forward", "train_step")})
         flags.append(vp.flags)
-    assert not any(f & Lw.FLAG_LAYOUT_APPROX for f in flags)
     assert any(f & Lw.FLAG_ALTERNATE for f in flags)
 
 
