@@ -193,7 +193,7 @@ def reference_throughput(keys, seconds=None):
         warm = time.perf_counter() - t
         n = len(keys)
         if seconds is not None:
-            n = max(cores, min(len(keys), int(cores * seconds / max(warm, 1e-3))))
+            n = min(len(keys), max(4 * cores, int(cores * seconds / max(warm, 1e-3))))
         t = time.perf_counter()
         res = pool.map(_ref_eval, keys[:n], chunksize=1)
         dt = time.perf_counter() - t
@@ -224,7 +224,7 @@ def run_reference(args, world, rank):
         keys = [inds[(start + k) % len(inds)]["key"] for k in range(args.pop)]
         if per_step is None:
             # size the sample once so the whole run stays within minutes
-            r, cores, n, dt, _ = reference_throughput(keys, seconds=4.0)
+            r, cores, n, dt, _ = reference_throughput(keys, seconds=8.0)
             per_step = n
         else:
             r, cores, n, dt, _ = reference_throughput(keys[:per_step])

@@ -209,6 +209,7 @@ class DeviceEvaluator:
         self.last_timing = {}
         self.last_plan_bytes = 0
         self.last_device_ms = 0.0
+        self.launches = 0          # gevo_eval launches so far (bench: gpu_launches)
 
     def _learn_layout(self, res, order):
         """Remember which launch slots shared an SM (records carry the SM id
@@ -357,6 +358,7 @@ class DeviceEvaluator:
             # a device failure in either half is loud, never a missing fitness
             raise failed[min(failed)]
         used = sorted(box)
+        self.launches += sum(launches[k][0] for k in used)
         if any(launches[k][0] > 1 for k in used):
             # consecutive launches (scratch budget): kernel time summed per
             # half; the halves run concurrently
