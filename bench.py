@@ -172,6 +172,16 @@ def _ref_eval(key):
     return f.cost, f.error, f.valid
 
 
+def _one_blas_thread():
+    """Pool initializer: one OpenBLAS thread per worker process (numpy was
+    imported before the fork, so the environment variable alone is too late)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except ImportError:
+        pass
+
+
 def reference_throughput(keys, seconds=None):
     """evotir.fitness.evaluate over `keys` in a process pool with one process
     per host core and OPENBLAS_NUM_THREADS=1 (the reference's own thread pool
@@ -187,7 +197,7 @@ def reference_throughput(keys, seconds=None):
     if _REF_WL is None:
         _REF_WL = F.build_2fcnet_workload()          # inherited by the forked workers
     ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
+    with ctx.Pool(cores, initializer=_one_blas_thread) as pool:
         t = time.perf_counter()
         pool.map(_ref_eval, keys[:cores], chunksize=1)      # warm every worker
         warm = time.perf_counter() - t
