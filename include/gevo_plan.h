@@ -3,8 +3,9 @@
  * A plan is one flat blob per generation:
  *   gevo_plan_header | gevo_instr[n_instr] | gevo_prog[n_prog] | double consts[n_const]
  * Each gevo_prog is one individual (one mutated program): index ranges into
- * the instruction table for its @train_step (step 0 / steps >= 1, which can
- * differ only in operand layouts) and its @forward, plus its arena size.
+ * the instruction table for its @train_step (step 0 and up to two more
+ * layouts of its weights, which can differ only in operand layouts) and its
+ * @forward, plus its arena size.
  *
  * Scratch is two-tier: values small enough live in the CTA's shared memory
  * (GEVO_BUF_SMEM, reused by liveness), the rest in the individual's HBM arena
@@ -24,7 +25,7 @@
 #include <stdint.h>
 
 #define GEVO_PLAN_MAGIC 0x47455650u /* "GEVP" */
-#define GEVO_PLAN_VERSION 1
+#define GEVO_PLAN_VERSION 2
 #define GEVO_MAXR 6        /* max tensor rank */
 #define GEVO_MAXP 8        /* max function params / returns */
 
@@ -106,9 +107,29 @@ typedef struct {
 } gevo_instr;                         /* 224 bytes */
 
 /* gevo_prog.flags */
-/* bit 0 is unused: a variant whose returned layouts have no period <= 2 is
- * refused by the lowering (plan.UnsupportedVariant), never approximated */
-#define GEVO_FLAG_ALTERNATE 2         /* steps >= 1: odd -> train1, even -> train0 */
+/* bits 0..1: which program each training step runs.  The weights' numpy
+ * layouts can change from step to step (a mutated train_step may return a
+ * transposed or broadcast view), and every program is lowered for the
+ * layouts it reads; the lowering follows the layouts to their cycle
+ * (plan.lower_variant) and a variant whose cycle does not fit these four is
+ * refused (plan.UnsupportedVariant), never approximated.  Step 0 always runs
+ * train0 (C-ordered initial weights). */
+#define GEVO_SCHED_MASK 3
+#define GEVO_SCHED_STEADY1 0          /* steps >= 1: train1 */
+#define GEVO_SCHED_STEADY2 1          /* step 1: train1; steps >= 2: train2 */
+#define GEVO_SCHED_ALT01 2            /* steps >= 1: odd -> train1, even -> train0 */
+#define GEVO_SCHED_ALT12 3            /* steps >= 1: odd -> train1, even -> train2 */
+#define GEVO_FLAG_ALTERNATE GEVO_SCHED_ALT01   /* (plan version 1 name) */
+/* In-place weights (training, GEVO_SCHED_STEADY1 only): bit w of
+ * (flags >> GEVO_FLAG_INPLACE_SHIFT) & 0x3F set means weight w is updated in
+ * place by train1 -- it lives in block 0 of the individual's weight
+ * ping-pong from step 0 on (step 0 reads the shared initial weights and
+ * writes block 0; later steps read and write block 0).  The lowering proves
+ * it safe (plan.inplace_weights): one instruction writes the return, reading
+ * the parameter only at the words it overwrites, and nothing after it reads
+ * the parameter.  Halves the weights' HBM/L2 footprint (w1: 200 KB). */
+#define GEVO_FLAG_INPLACE_SHIFT 2
+#define GEVO_FLAG_INPLACE(f) (((f) >> GEVO_FLAG_INPLACE_SHIFT) & 0x3F)
 /* Score parts (prediction mode only): an individual's scored batches are
  * independent (fitness.py:361-368), so n_parts programs may share one
  * result_slot, part j scoring batches j, j + n_parts, ...  gevo_eval merges
@@ -129,7 +150,8 @@ typedef struct {
   int32_t flags;
   int32_t param_off[GEVO_MAXP];       /* exec-once: offsets into params blob */
   int32_t out_off[GEVO_MAXP];         /* exec-once: offsets into outs blob */
-} gevo_prog;                          /* 112 bytes */
+  int32_t train2, train2_n;           /* @train_step for a third layout (GEVO_SCHED_*) */
+} gevo_prog;                          /* 120 bytes */
 
 typedef struct {
   uint32_t magic, version;

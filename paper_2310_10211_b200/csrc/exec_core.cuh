@@ -42,8 +42,13 @@ __device__ __forceinline__ int64_t addr(const gevo_operand& o, const int* idx, i
 }
 
 // numpy float64 maximum: NaN propagates, otherwise the first of equal values
+// np.maximum on x86 (MAXPD): a when a > b or a is NaN, else b -- so the
+// second operand on ties, which decides signed zeros: maximum(-0.0, 0.0) is
+// 0.0 and maximum(0.0, -0.0) is -0.0 (tests/golden/edge_cases.json.gz,
+// recorded from the reference).  np.max's running reduction keeps the same
+// rule (the later element wins a tie: probed on numpy 2.3.5).
 __device__ __forceinline__ double np_fmax(double a, double b) {
-  return (a >= b || a != a) ? a : b;
+  return (a > b || a != a) ? a : b;
 }
 
 // numpy trunc(x).astype(int64) on x86: NaN/inf/out of range -> INT64_MIN

@@ -115,7 +115,8 @@ int parse_plan(gevo_ctx* ctx, const void* plan, size_t bytes, PlanView* v) {
   for (int i = 0; i < h->n_prog; ++i) {
     const gevo_prog& p = progs[i];
     auto ok = [&](int o, int n) { return o >= 0 && n >= 0 && o + n <= h->n_instr; };
-    if (!ok(p.train0, p.train0_n) || !ok(p.train1, p.train1_n) || !ok(p.fwd, p.fwd_n))
+    if (!ok(p.train0, p.train0_n) || !ok(p.train1, p.train1_n) || !ok(p.train2, p.train2_n) ||
+        !ok(p.fwd, p.fwd_n))
       return fail(ctx, GEVO_E_ARG, "prog instruction range out of bounds");
     if (p.arena_off < 0 || p.arena_off > h->total_elems)
       return fail(ctx, GEVO_E_ARG, "prog arena offset out of bounds");

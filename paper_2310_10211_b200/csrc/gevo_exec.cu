@@ -953,6 +953,19 @@ __device__ const gevo_instr* stage(gevo_instr* cache, const gevo_instr* g, int n
   return cache;
 }
 
+// every weight finite: weight i at (inplace bit i ? blk0 : cur) + wofs[i]
+// (its extent runs to the next weight's offset; padding words stay zero)
+__device__ bool weights_finite(const double* blk0, const double* cur, int inplace, const int32_t* wofs,
+                               int nw, int elems) {
+  int bad = 0;
+  for (int w = 0; w < nw; ++w) {
+    const double* b = ((inplace >> w) & 1) ? blk0 : cur;
+    const int lo = w == 0 ? 0 : wofs[w], hi = w + 1 < nw ? wofs[w + 1] : elems;
+    for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) bad |= !isfinite(b[i]);
+  }
+  return !__syncthreads_or(bad);
+}
+
 __device__ bool all_finite(const double* w, int n) {
   int bad = 0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) bad |= !isfinite(w[i]);
@@ -985,6 +998,9 @@ eval_kernel(EvalArgs args) {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
 
   const double* final_w = args.init_weights;
+  // weights updated in place (GEVO_FLAG_INPLACE): they live in block 0
+  const int inplace = (args.mode == GEVO_MODE_TRAIN && args.steps > 0 &&
+                       (P.flags & GEVO_SCHED_MASK) == GEVO_SCHED_STEADY1) ? GEVO_FLAG_INPLACE(P.flags) : 0;
   if (args.mode == GEVO_MODE_TRAIN && args.steps > 0) {
     // A step stores each returned weight in its numpy layout; a broadcast
     // (stride-0) or otherwise compact return covers only part of its slot.
@@ -995,42 +1011,63 @@ eval_kernel(EvalArgs args) {
     const gevo_instr* t0 = stage(cache, args.instrs + P.train0, P.train0_n);
     const gevo_instr* cur = t0;
     const int check = args.check_every > 0 ? args.check_every : 1;
-    const bool alternate = P.flags & GEVO_FLAG_ALTERNATE;
+    // step 0 reads C-ordered weights (train0); later steps read the layout
+    // the previous step stored, so the program follows the layout cycle
+    // (gevo_plan.h GEVO_SCHED_*): train1 for every s >= 1; train1 on odd and
+    // train0 on even steps (C <-> L0); train1 at step 1 then train2; train1
+    // on odd and train2 on even steps >= 2 (L0 <-> L1)
+    const int sched = P.flags & GEVO_SCHED_MASK;
+    const int pstart[3] = {P.train0, P.train1, P.train2};
+    const int plen[3] = {P.train0_n, P.train1_n, P.train2_n};
+    int pid = 0;
     for (int s = 0; s < args.steps; ++s) {
-      // step 0 reads C-ordered weights (train0); later steps read the layout
-      // the previous step stored: train1 for every s >= 1, or -- when that
-      // layout flips back to C order each step (GEVO_FLAG_ALTERNATE) --
-      // train1 on odd and train0 on even steps
-      if (s >= 1 && P.train1 != P.train0 && (s == 1 || alternate)) {
-        const bool odd = s & 1;
-        __syncthreads();
-        cur = (odd || !alternate) ? stage(cache, args.instrs + P.train1, P.train1_n)
-                                  : stage(cache, args.instrs + P.train0, P.train0_n);
+      int want = 0;
+      if (s > 0) {
+        switch (sched) {
+          case GEVO_SCHED_STEADY1: want = 1; break;
+          case GEVO_SCHED_STEADY2: want = s == 1 ? 1 : 2; break;
+          case GEVO_SCHED_ALT01: want = (s & 1) ? 1 : 0; break;
+          default: want = (s & 1) ? 1 : 2; break;
+        }
+      }
+      if (want != pid) {
+        if (pstart[want] != pstart[pid]) {
+          __syncthreads();
+          cur = stage(cache, args.instrs + pstart[want], plen[want]);
+        }
+        pid = want;
       }
       const double* win = (s == 0) ? args.init_weights : wbuf[s & 1];
       double* wout = wbuf[(s + 1) & 1];
+      // in-place weights live in block 0 (read from it from step 1 on)
+      const double* win_ip = (s == 0) ? args.init_weights : wbuf[0];
       const int b = s % args.train_nb;
       if (threadIdx.x == 0) {
         S.base[GEVO_BUF_ARENA] = scratch;
         S.base[GEVO_BUF_SMEM] = smem_arena;
         S.base[GEVO_BUF_CONST] = const_cast<double*>(consts);
         for (int i = 0; i < nw; ++i) {
-          S.base[GEVO_BUF_PARAM0 + i] = const_cast<double*>(win) + args.wofs[i];
-          S.base[GEVO_BUF_OUT0 + i] = wout + args.wofs[i];
+          const bool ip = (inplace >> i) & 1;
+          S.base[GEVO_BUF_PARAM0 + i] = const_cast<double*>(ip ? win_ip : win) + args.wofs[i];
+          S.base[GEVO_BUF_OUT0 + i] = (ip ? wbuf[0] : wout) + args.wofs[i];
         }
         S.base[GEVO_BUF_PARAM0 + nw] = const_cast<double*>(args.train_x) + (int64_t)b * args.x_elems;
         S.base[GEVO_BUF_PARAM0 + nw + 1] = const_cast<double*>(args.train_y) + (int64_t)b * args.y_elems;
       }
       __syncthreads();
-      run_instrs(S, cur, (s == 0 || (alternate && !(s & 1))) ? P.train0_n : P.train1_n, dstage, args.prof);
+      run_instrs(S, cur, plen[pid], dstage, args.prof);
       steps_run = s + 1;
-      if ((s + 1) % check == 0 && !all_finite(wout, args.weight_elems)) {
+      if ((s + 1) % check == 0 &&
+          !(inplace ? weights_finite(wbuf[0], wout, inplace, args.wofs, nw, args.weight_elems)
+                    : all_finite(wout, args.weight_elems))) {
         status = GEVO_STATUS_NONFINITE_WEIGHTS;
         break;
       }
     }
     final_w = wbuf[args.steps & 1];
-    if (status == GEVO_STATUS_OK && !all_finite(final_w, args.weight_elems))
+    if (status == GEVO_STATUS_OK &&
+        !(inplace ? weights_finite(wbuf[0], final_w, inplace, args.wofs, nw, args.weight_elems)
+                  : all_finite(final_w, args.weight_elems)))
       status = GEVO_STATUS_NONFINITE_WEIGHTS;
     __syncthreads();
   }
@@ -1048,7 +1085,7 @@ eval_kernel(EvalArgs args) {
         S.base[GEVO_BUF_SMEM] = smem_arena;
         S.base[GEVO_BUF_CONST] = const_cast<double*>(consts);
         for (int i = 0; i < nw; ++i)
-          S.base[GEVO_BUF_PARAM0 + i] = const_cast<double*>(final_w) + args.wofs[i];
+          S.base[GEVO_BUF_PARAM0 + i] = const_cast<double*>(((inplace >> i) & 1) ? wbuf[0] : final_w) + args.wofs[i];
         S.base[GEVO_BUF_PARAM0 + nw] = const_cast<double*>(args.score_x) + (int64_t)b * args.x_elems;
         S.base[GEVO_BUF_OUT0] = probs;
         S.wrong = 0;
@@ -1087,7 +1124,11 @@ eval_kernel(EvalArgs args) {
   }
   if (args.final_weights != nullptr) {
     double* dst = args.final_weights + (int64_t)P.result_slot * args.weight_elems;
-    for (int i = threadIdx.x; i < args.weight_elems; i += blockDim.x) dst[i] = final_w[i];
+    for (int w = 0; w < nw; ++w) {
+      const double* b = ((inplace >> w) & 1) ? wbuf[0] : final_w;
+      const int lo = w == 0 ? 0 : args.wofs[w], hi = w + 1 < nw ? args.wofs[w + 1] : args.weight_elems;
+      for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) dst[i] = b[i];
+    }
   }
 }
 

@@ -146,6 +146,15 @@ def _collect(jobs):
     return pos, res
 
 
+def _arena_budget() -> float:
+    """GEVO_B200_ARENA_GB (default 64) in bytes of requested scratch.  The
+    library's buffers grow to request + 25 % (DevBuf::ensure, gevo_abi.cu),
+    so the grouping budget is the knob / 1.25: the device footprint stays
+    within the figure (approximately: growth briefly holds the old buffer
+    too, stream-ordered)."""
+    return float(os.environ.get("GEVO_B200_ARENA_GB", "64")) * 1e9 / 1.25
+
+
 def lower_all(variants, cost_table, training, steps=600):
     """lower_variant over a list (None entries stay None), in the process
     pool when the list is large."""
@@ -402,7 +411,7 @@ class DeviceEvaluator:
         """[g0, g1) ranges of `lowered` whose device scratch (arena, probs
         and weight ping-pong per individual) fits GEVO_B200_ARENA_GB (default
         64) split over `shares` concurrent launches."""
-        budget = float(os.environ.get("GEVO_B200_ARENA_GB", "64")) * 1e9 / max(1, shares)
+        budget = _arena_budget() / max(1, shares)
         fixed = 8 * (((self.batch * self.classes + 15) & ~15) + 2 * ((self.weight_elems + 15) & ~15))
         groups, g0, acc = [], 0, 0
         for k, v in enumerate(lowered):
@@ -429,7 +438,7 @@ class DeviceEvaluator:
         parts = max(1, min(n_score, (2 * self.n_sms) // max(n, n_total or 0)))
         per = sum(8 * ((v.arena + 15) & ~15) for v in lowered) + \
             8 * n * (self.batch * self.classes + 2 * self.weight_elems + 48)
-        budget = float(os.environ.get("GEVO_B200_ARENA_GB", "64")) * 1e9 / max(1, shares)
+        budget = _arena_budget() / max(1, shares)
         while parts > 1 and parts * per > budget:
             parts -= 1
         return parts

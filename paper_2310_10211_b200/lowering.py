@@ -55,7 +55,7 @@ CMP_CODES = {"eq": 5, "ne": 6, "lt": 7, "le": 8, "gt": 9, "ge": 10}
 R_SUM_PAIRWISE, R_SUM_SEQ, R_MAX = 0, 1, 2
 D_FMA_CHAIN, D_ACC8_TREE, D_SEQ_NOFMA, D_ACC8_TAIL = 0, 1, 2, 3
 
-PLAN_MAGIC, PLAN_VERSION = 0x47455650, 1
+PLAN_MAGIC, PLAN_VERSION = 0x47455650, 2
 
 _OPERAND = [("buf", "<i4"), ("off", "<i4"), ("st", "<i4", (MAXR,))]
 INSTR_DTYPE = np.dtype([
@@ -68,16 +68,20 @@ PROG_DTYPE = np.dtype([
     ("train1_n", "<i4"), ("fwd", "<i4"), ("fwd_n", "<i4"),
     ("const_off", "<i4"), ("result_slot", "<i4"), ("arena_off", "<i8"),
     ("arena_elems", "<i4"), ("flags", "<i4"),
-    ("param_off", "<i4", (MAXP,)), ("out_off", "<i4", (MAXP,))], align=True)
+    ("param_off", "<i4", (MAXP,)), ("out_off", "<i4", (MAXP,)),
+    ("train2", "<i4"), ("train2_n", "<i4")], align=True)
 HEADER_DTYPE = np.dtype([
     ("magic", "<u4"), ("version", "<u4"), ("n_instr", "<i4"),
     ("n_prog", "<i4"), ("n_const", "<i4"), ("weight_elems", "<i4"),
     ("n_weights", "<i4"), ("wofs", "<i4", (MAXP,)), ("max_arena", "<i4"),
     ("max_smem", "<i4"), ("total_elems", "<i8")], align=True)
-assert INSTR_DTYPE.itemsize == 224 and PROG_DTYPE.itemsize == 112
+assert INSTR_DTYPE.itemsize == 224 and PROG_DTYPE.itemsize == 120
 assert HEADER_DTYPE.itemsize == 80
 
-FLAG_ALTERNATE = 2         # layouts alternate: steps >= 1 odd -> train1, even -> train0
+# step schedules (gevo_plan.h GEVO_SCHED_*, flags bits 0..1)
+SCHED_STEADY1, SCHED_STEADY2, SCHED_ALT01, SCHED_ALT12 = 0, 1, 2, 3
+FLAG_ALTERNATE = SCHED_ALT01   # steps >= 1: odd -> train1, even -> train0
+FLAG_INPLACE_SHIFT = 2     # bits 2..7: weights train1 updates in place (plan.inplace_weights)
 
 _NP_DTYPE = {K_F64: np.float64, K_I64: np.int64, K_I1: np.int64}
 
@@ -157,13 +161,55 @@ def dot_modes(a: Val, b: Val):
     corner = m - m % 4 if n % 8 and m % 4 else m
     # cblas row-major -> col-major: A' = B (trans_b), B' = A (trans_a)
     tn = trans_b and not trans_a
-    small = m * n * k <= 1_000_000 and (not tn or (m * n <= 1200 and k >= 32))
+    small = _small_kernel(m, k, n, tn)
     if small and tn:
         return D_ACC8_TREE, n - n % 8, D_ACC8_TREE, corner
-    if not trans_a and not trans_b and n % 8 and k >= 16:
-        # the n % 8 edge columns of the NN kernel: 8 lane chains once K >= 16
+    if small and not trans_a and not trans_b and n % 8 and k >= 16:
+        # the n % 8 edge columns of the NN small kernel: 8 lane chains once
+        # K >= 16 (the blocked kernels below keep one chain per output)
         return D_FMA_CHAIN, n - n % 8, D_ACC8_TREE, corner
     return D_FMA_CHAIN, n, D_FMA_CHAIN, m
+
+
+def _small_kernel(m, k, n, tn) -> bool:
+    """OpenBLAS's small-matrix permit (SkylakeX dgemm): M*N*K <= 1e6, and
+    for TN problems only small outputs with K >= 32.  Everything else takes
+    the blocked GEMM driver."""
+    return m * n * k <= 1_000_000 and (not tn or (m * n <= 1200 and k >= 32))
+
+
+GEMM_Q = 384   # OpenBLAS SkylakeX DGEMM_DEFAULT_Q: the blocked driver's K block
+
+
+def dot_kblocks(a: Val, b: Val):
+    """K ranges the blocked GEMM driver accumulates separately: each block
+    is a fresh k-ordered fma chain, and C = C + block rounds once per block
+    (beta = 0, alpha = 1).  The driver's split (level3_thread.c, numpy's
+    default threaded OpenBLAS): a remainder >= 2Q takes Q, one in (Q, 2Q)
+    is halved, (r + 1) / 2.  Probed here on numpy 2.3.5 / OpenBLAS 0.3.30
+    (tests/test_dot_orders.py::test_blocked_k_split); the single-threaded
+    driver rounds the half up to a multiple of 16 instead, which agrees on
+    every K the workloads reach (the CNN's K = 480 -> 240 + 240).  Small-
+    kernel problems and gemv shapes are one block."""
+    m, k = a.shape
+    n = b.shape[1]
+    if a.kind != K_F64 or m == 1 or k == 1 or n == 1 or k <= GEMM_Q:
+        return [(0, k)]
+    sa = _blas_strides(a.st, m, k)
+    sb = _blas_strides(b.st, k, n)
+    tn = (not _blas2d(sb[0], sb[1], n)) and _blas2d(sa[0], sa[1], k)
+    if _small_kernel(m, k, n, tn):
+        return [(0, k)]
+    out, ls = [], 0
+    while ls < k:
+        ml = k - ls
+        if ml >= 2 * GEMM_Q:
+            ml = GEMM_Q
+        elif ml > GEMM_Q:
+            ml = (ml + 1) // 2
+        out.append((ls, ls + ml))
+        ls += ml
+    return out
 
 
 def _pad_dims(shape):
@@ -339,6 +385,9 @@ class _Builder:
             return out
         if code == "dot":
             a, b = ins
+            blocks = dot_kblocks(a, b)
+            if len(blocks) > 1:
+                return self.blocked_dot(op, a, b, blocks, shape, kind)
             out = self.result_val(op, shape, L.c_strides(shape), kind)
             m1, split, m2, xrow = dot_modes(a, b)
             corner = xrow + 1 if xrow < a.shape[0] else 0
@@ -375,6 +424,28 @@ class _Builder:
                       aux2=list(a.shape))
             return out
         raise LoweringError(f"cannot lower opcode {code!r}")
+
+    def blocked_dot(self, op, a, b, blocks, shape, kind):
+        """A blocked-driver dot (dot_kblocks): one k-ordered chain per K
+        block into scratch, folded as C = C + block (the add rounds once,
+        like the driver's C update); fuse_dot_epilogues then makes each add
+        the epilogue of its block's dot."""
+        m, n = shape
+        acc = None
+        for j, (k0, k1) in enumerate(blocks):
+            av = Val(a.buf, a.off + k0 * a.st[1], (m, k1 - k0), a.st, a.kind, a.alloc)
+            bv = Val(b.buf, b.off + k0 * b.st[0], (k1 - k0, n), b.st, b.kind, b.alloc)
+            part = self.fresh(shape, L.c_strides(shape), kind, m * n)
+            self.emit(OP_DOT, D_FMA_CHAIN, part, [av, bv], aux=[k1 - k0, n, D_FMA_CHAIN, 0])
+            if acc is None:
+                acc = part
+                continue
+            last = j == len(blocks) - 1
+            out = self.result_val(op, shape, L.c_strides(shape), kind) if last else \
+                self.fresh(shape, L.c_strides(shape), kind, m * n)
+            self.emit(OP_BINARY, B_CODES["add"], out, [acc, part])
+            acc = out
+        return acc
 
     def reshape(self, a: Val, shape, idx):
         st = L.reshape_view(a.shape, a.st, shape)

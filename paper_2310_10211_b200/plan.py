@@ -7,12 +7,14 @@ that the device executor walks, one CTA per individual.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import layout as L
-from .lowering import (BUF_OUT0, FLAG_ALTERNATE, HEADER_DTYPE,
+from .lowering import (BUF_OUT0, FLAG_ALTERNATE, FLAG_INPLACE_SHIFT, HEADER_DTYPE, MAXP,
+                       SCHED_ALT01, SCHED_ALT12, SCHED_STEADY1, SCHED_STEADY2,
                        INSTR_DTYPE, PLAN_MAGIC, PLAN_VERSION, PROG_DTYPE,
                        consts_to_words, encode_instrs, lower_function,
                        static_cost)
@@ -39,6 +41,7 @@ class VariantPlan:
     fwd_cost: float
     w_train: float = 0.0          # fn_weight(train1) / fn_weight(fwd), computed where
     w_fwd: float = 0.0            # the variant is lowered (a pool worker), not in the parent
+    train2: np.ndarray | None = None   # third layout's program (GEVO_SCHED_STEADY2 / ALT12)
 
 
 def _count(shape):
@@ -58,7 +61,7 @@ def lower_variant(functions: dict, cost_table=None, training=True,
     arena = 0
     smem = 0
     flags = 0
-    t0 = t1 = None
+    t0 = t1 = t2 = None
     train_cost = 0.0
     fwd_layouts = weight_layouts
     if training:
@@ -68,35 +71,54 @@ def lower_variant(functions: dict, cost_table=None, training=True,
         low0 = lower_function(ts, c_layout, cost_table=cost_table)
         train_cost = low0.cost
         L0 = list(low0.ret_strides)
-        final = L0                          # layout of the weights after `steps`
-        if L0 == list(c_layout[:nw]):
-            low1 = low0                     # C order is a fixed point
-        else:
+        low2 = None
+        C = list(c_layout[:nw])
+
+        def lower_for(lay):
             layouts = list(c_layout)
-            layouts[:nw] = L0
-            low1 = lower_function(ts, layouts, cost_table=cost_table)
+            layouts[:nw] = lay
+            return lower_function(ts, layouts, cost_table=cost_table)
+        # follow the weights' layouts to their cycle: step s reads the layout
+        # step s-1 stored (gevo_plan.h GEVO_SCHED_*)
+        if L0 == C:
+            low1, sched, after = low0, SCHED_STEADY1, lambda n: L0
+        else:
+            low1 = lower_for(L0)
             L1 = list(low1.ret_strides)
             if L1 == L0:
-                final = L0                  # fixed point from step 1 on
-            elif L1 == list(c_layout[:nw]):
+                sched, after = SCHED_STEADY1, lambda n: L0
+            elif L1 == C:
                 # period 2: even steps read C order (train0) and store L0,
                 # odd steps read L0 (train1) and store C order
-                flags |= FLAG_ALTERNATE
-                final = L0 if (steps - 1) % 2 == 0 else L1
+                sched, after = SCHED_ALT01, lambda n: L0 if (n - 1) % 2 == 0 else L1
             else:
-                # the weights' numpy layouts do not settle within two steps
-                # (C -> L0 -> L1 with L1 not in {C, L0}); never seen in any
-                # recorded population.  The summation orders of later steps
-                # depend on those layouts, so refuse loudly rather than run
-                # step >= 2 with the wrong program.
-                raise UnsupportedVariant(
-                    "train_step returns weight layouts with no period <= 2 "
-                    f"(step 0 -> {L0}, step 1 -> {L1}); not supported by the device executor")
+                low2 = lower_for(L1)
+                L2 = list(low2.ret_strides)
+                if L2 == L1:
+                    # settles from step 2: C -> L0 -> L1 -> L1 ...
+                    sched, after = SCHED_STEADY2, lambda n: L0 if n == 1 else L1
+                elif L2 == L0:
+                    # period 2 from step 1: L0 -> L1 -> L0 ...
+                    sched, after = SCHED_ALT12, lambda n: L0 if (n - 1) % 2 == 0 else L1
+                else:
+                    # C -> L0 -> L1 -> L2 with L2 not in {L0, L1}: never seen
+                    # in any recorded population.  The summation orders of
+                    # later steps depend on those layouts, so refuse loudly
+                    # rather than run any step with the wrong program.
+                    raise UnsupportedVariant(
+                        "train_step returns weight layouts that do not cycle within three steps "
+                        f"(step 0 -> {L0}, step 1 -> {L1}, step 2 -> {L2}); not supported by "
+                        "the device executor")
+        flags |= sched
+        final = after(steps) if steps > 0 else C
         t0 = _encode_shifted(low0, consts)
         t1 = t0 if low1 is low0 else _encode_shifted(low1, consts)
-        arena = max(low0.arena_elems, low1.arena_elems)
-        smem = max(low0.smem_elems, low1.smem_elems)
-        fwd_layouts = final if steps > 0 else list(c_layout[:nw])
+        t2 = None if low2 is None else _encode_shifted(low2, consts)
+        if sched == SCHED_STEADY1 and INPLACE:
+            flags |= inplace_weights(t1, nw) << FLAG_INPLACE_SHIFT
+        arena = max(low0.arena_elems, low1.arena_elems, low2.arena_elems if low2 else 0)
+        smem = max(low0.smem_elems, low1.smem_elems, low2.smem_elems if low2 else 0)
+        fwd_layouts = final
     fw = functions["forward"]
     nwf = len(fw.params) - 1
     f_layout = [L.c_strides(tuple(t.shape)) for _, t in fw.params]
@@ -107,7 +129,79 @@ def lower_variant(functions: dict, cost_table=None, training=True,
     arena = max(arena, lowf.arena_elems)
     smem = max(smem, lowf.smem_elems)
     return VariantPlan(t0, t1, f, consts_to_words(consts), arena, smem, flags,
-                       train_cost, lowf.cost, fn_weight(t1), fn_weight(f))
+                       train_cost, lowf.cost, fn_weight(t1), fn_weight(f), t2)
+
+
+# in-place weight updates (inplace_weights); GEVO_B200_INPLACE=0 turns them off
+INPLACE = os.environ.get("GEVO_B200_INPLACE", "1") != "0"
+_NIN = {1: 1, 2: 2, 3: 3, 4: 1, 5: 2, 6: 2, 8: 2}   # main operands per op class
+
+
+def inplace_weights(arr, nw) -> int:
+    """Bit w set: @train_step (the program of steps >= 1) may update weight w
+    in place -- its parameter and its return sharing one HBM block instead
+    of ping-ponging (gevo_plan.h GEVO_FLAG_INPLACE_SHIFT).  Safe when
+      * exactly one instruction W writes return w, and W is elementwise
+        (UNARY / BINARY / SELECT, fused chains included) or a DOT;
+      * W reads parameter w only at the very word it writes (offset and
+        strides equal to its output's), a DOT only in its epilogue;
+      * no instruction after W reads parameter w.
+    Then every word of the parameter is read, at the latest, by the thread
+    that overwrites it, inside W.  The layout the next step reads is the one
+    W stores either way (the returned layout is a fixed point of the
+    program of steps >= 1).  `arr` is the encoded table, EXT records
+    included."""
+    groups, k = [], 0
+    n = len(arr)
+    while k < n:
+        r = arr[k]
+        op = int(r["op"])
+        n_ext = int(r["aux2"][0]) if op == 5 else (int(r["aux2"][4]) if op in (1, 2, 3, 8) else 0)
+        groups.append((k, n_ext))
+        k += 1 + n_ext
+    mask = 0
+    for w in range(nw):
+        P, O = 2 + w, 2 + MAXP + w
+        writers = [g for g, (k, _) in enumerate(groups) if int(arr[k]["out"]["buf"]) == O]
+        if len(writers) != 1:
+            continue
+        g_w = writers[0]
+        W = arr[groups[g_w][0]]
+        op = int(W["op"])
+        if op not in (1, 2, 3, 5):
+            continue
+        rank = 2 if op == 5 else int(W["rank"])
+
+        def key(v, is_ext):
+            # the word an operand reads for output index (r, c) of a rank <= 2
+            # instruction (EXT operands are 2-D views, main operands of a
+            # rank-1 instruction address c with st[0]); rank > 2: the N-d walk
+            st = [int(x) for x in v["st"]]
+            if rank > 2:
+                return int(v["off"]), tuple(st[:rank])
+            if is_ext or rank == 2:
+                return int(v["off"]), (st[0], st[1])
+            return int(v["off"]), (0, st[0] if rank == 1 else 0)
+        out_key = key(W["out"], False)
+        ok = True
+        for g in range(g_w, len(groups)):
+            k, e = groups[g]
+            rec = arr[k]
+            reads = [rec["in"][j] for j in range(_NIN.get(int(rec["op"]), 0))]
+            ext = [arr[k + 1 + x]["in"][j] for x in range(e) for j in range(3)]
+            if g > g_w:
+                ok = not any(int(v["buf"]) == P for v in reads + ext)
+            elif op == 5 and any(int(v["buf"]) == P for v in reads):
+                ok = False
+            else:
+                ok = all(key(v, x) == out_key
+                         for v, x in ([] if op == 5 else [(v, False) for v in reads]) +
+                         [(v, True) for v in ext] if int(v["buf"]) == P)
+            if not ok:
+                break
+        if ok:
+            mask |= 1 << w
+    return mask
 
 
 def _encode_shifted(low, pool):
@@ -285,6 +379,13 @@ def build_population_plan(variants: list[VariantPlan], weight_shapes,
                     p["train1"], p["train1_n"] = n_instr, len(b)
                     instr_chunks.append(b)
                     n_instr += len(b)
+                if v.train2 is None:
+                    p["train2"], p["train2_n"] = p["train1"], p["train1_n"]
+                else:
+                    c = v.train2
+                    p["train2"], p["train2_n"] = n_instr, len(c)
+                    instr_chunks.append(c)
+                    n_instr += len(c)
             f = v.fwd
             p["fwd"], p["fwd_n"] = n_instr, len(f)
             instr_chunks.append(f)

@@ -44,8 +44,8 @@ def test_null_context_is_an_error_not_a_crash():
 def test_plan_struct_sizes_match_header():
     from paper_2310_10211_b200 import lowering as Lw
     hdr = open(os.path.join(ROOT, "include", "gevo_plan.h")).read()
-    assert "/* 224 bytes */" in hdr and "/* 112 bytes */" in hdr
-    assert Lw.INSTR_DTYPE.itemsize == 224 and Lw.PROG_DTYPE.itemsize == 112
+    assert "/* 224 bytes */" in hdr and "/* 120 bytes */" in hdr
+    assert Lw.INSTR_DTYPE.itemsize == 224 and Lw.PROG_DTYPE.itemsize == 120
 
 
 def _c_sizeof(types):

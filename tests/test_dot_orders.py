@@ -102,3 +102,39 @@ def test_dot_orders_k_thresholds():
         for k in list(range(2, 41)) + [48, 64, 100]:
             for ka, kb in (("C", "C"), ("C", "T"), ("T", "C"), ("T", "T")):
                 check(rng, m, k, n, ka, kb)
+
+
+def _chain(A, B, i, j, k0, k1):
+    acc = 0.0
+    for t in range(k0, k1):
+        acc = fma(A[i, t], B[t, j], acc)
+    return acc
+
+
+@pytest.mark.parametrize("shape", [(1600, 480, 80), (1600, 800, 24), (20000, 72, 12),
+                                   (20000, 48, 12), (6400, 288, 48)])
+def test_blocked_k_split(shape):
+    """Problems past the small-matrix permit (M*N*K > 1e6) take OpenBLAS's
+    blocked driver: one k-ordered chain per output inside each K block
+    (no 8-lane edge kernels, whatever n % 8), blocks added in order
+    (lowering.dot_kblocks).  Found by the full-size CNN's probabilities:
+    (1600, 480, 80) splits 240 + 240; (102400, 72, 12) keeps chains in its
+    n % 8 = 4 edge columns."""
+    m, k, n = shape
+    rng = np.random.default_rng(m + k + n)
+    A, B = rng.standard_normal((m, k)), rng.standard_normal((k, n))
+    C = A @ B
+    a = Val(0, 0, A.shape, elem_strides(A), Lw.K_F64)
+    b = Val(0, 0, B.shape, elem_strides(B), Lw.K_F64)
+    m0, split, m1, _ = Lw.dot_modes(a, b)
+    assert (m0, split, m1) == (Lw.D_FMA_CHAIN, n, Lw.D_FMA_CHAIN)
+    blocks = Lw.dot_kblocks(a, b)
+    assert blocks[0][0] == 0 and blocks[-1][1] == k
+    assert (len(blocks) > 1) == (k > Lw.GEMM_Q)
+    for i in (0, 1, m // 2, m - 1):
+        for j in sorted({0, n // 2, n - 4, n - 1}):
+            got = None
+            for k0, k1 in blocks:
+                p = _chain(A, B, i, j, k0, k1)
+                got = p if got is None else got + p
+            assert got == C[i, j], (shape, blocks, i, j)

@@ -260,3 +260,61 @@ def test_elementwise_walks_output_memory_order():
     assert all(Lw._addr_mode(v, (32, 784)) == Lw.AM_LINEAR for v in rec["in"])
     (got,), _ = emulate(fn, [a, b])
     assert np.array_equal(got, (a.T + b.T))
+
+
+def _emulate_steps(ts, weights, xb, yb, steps):
+    """Steps of train_step through the lowering, each program lowered for
+    the layouts the previous step stored (returns stay in their compact
+    layout, the OUT words feed the next step's PARAM buffers as on the
+    device).  Returns the weights' logical values and the layout sequence."""
+    nw = len(ts.returns)
+    lay = [L.c_strides(tuple(t.shape)) for _, t in ts.params]
+    bufs = [_words(w) for w in weights]
+    seen = []
+    for _ in range(steps):
+        seen.append([tuple(x) for x in lay[:nw]])
+        low = Lw.lower_function(ts, lay)
+        consts = Lw.consts_to_words(low.consts).view(np.int64).copy() if low.consts \
+            else np.zeros(1, dtype=np.int64)
+        mem = {Lw.BUF_ARENA: np.zeros(max(low.arena_elems, 1), dtype=np.int64),
+               Lw.BUF_CONST: consts,
+               Lw.BUF_SMEM: np.zeros(max(low.smem_elems, 1), dtype=np.int64)}
+        for k, b in enumerate(bufs + [_words(xb), _words(yb)]):
+            mem[Lw.BUF_PARAM0 + k] = b
+        for r, ty in enumerate(ts.return_types):
+            mem[Lw.BUF_OUT0 + r] = np.zeros(max(1, int(np.prod(ty.shape))), dtype=np.int64)
+        plan_emu.run(low.instrs, mem)
+        bufs = [mem[Lw.BUF_OUT0 + r] for r in range(nw)]
+        lay[:nw] = [tuple(s) for s in low.ret_strides]
+    vals = []
+    for r, ty in enumerate(ts.return_types):
+        shape = tuple(ty.shape)
+        v = plan_emu.gather({0: bufs[r]}, Lw.Val(0, 0, shape, lay[r], Lw.K_F64), shape)
+        vals.append(v.view(np.float64).reshape(shape))
+    return vals, seen
+
+
+def test_three_layout_schedule_ga_individual():
+    """ga512x50 individual 10822 stores a different weight layout after step
+    0 and after step 1 (C -> L0 -> L1 -> L1 ...): the device runs train0,
+    train1, then train2 (GEVO_SCHED_STEADY2).  Before the schedule it was
+    refused (no period <= 2) and the recorded run could not be replayed.
+    The layouts the schedule assumes are the ones each step reads, and the
+    emulated trajectory follows the oracle."""
+    from paper_2310_10211_b200.plan import lower_variant
+    ind = load("ga512x50.json.gz")["individuals"][10822]
+    fns = {k: dialect.parse_function(ind[k]) for k in ("forward", "train_step")}
+    vp = lower_variant(fns)
+    assert vp.flags & 3 == Lw.SCHED_STEADY2 and vp.train2 is not None
+    wl = W.build_2fcnet_workload(W.WorkloadConfig(steps=5, dataset=W.DatasetConfig(search_n=320,
+                                                                                   holdout_n=64)))
+    w0 = [wl.weights[n] for n in W.WEIGHT_NAMES]
+    xb, yb = wl.search_x[0], wl.search_y[0]
+    got, seen = _emulate_steps(fns["train_step"], w0, xb, yb, 5)
+    assert seen[1] != seen[0] and seen[2] != seen[1] and seen[2] == seen[3] == seen[4]
+    prog = OI.Program(fns["train_step"])
+    w = list(w0)
+    for _ in range(5):
+        w = prog(w + [xb, yb])
+    for g_, r_ in zip(got, w):
+        assert np.allclose(g_, r_, rtol=1e-9, atol=1e-12, equal_nan=True)

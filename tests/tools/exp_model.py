@@ -1,12 +1,16 @@
 """Host model of csrc/exp_np.cuh (SVML __svml_exp8_ha restated), built as a
 tiny C helper at test time (TEST TOOL).  Same constants, same operation
-order; compiled with -frounding-math so the round-toward-zero FMA is real."""
+order; compiled with -frounding-math so the round-toward-zero FMA is real.
+The rare range (|x| >= 1021 ln2) compiles the product's own exp_rare.h."""
 import ctypes
 import os
 import subprocess
 import tempfile
 
 import numpy as np
+
+CSRC = os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))),
+                    "paper_2310_10211_b200", "csrc")
 
 TOP = [4607182418800017408, 4607381810190059791, 4607590029391122811, 4607807467243790904, 4608034531892639509, 4608271649552348194, 4608519265307732519, 4608777843949196329, 4609047870845172685, 4609329852853191047, 4609624319271280859, 4609931822831497360, 4610252940737434541, 4610588275747672732, 4610938457307194503, 4611304142728892634]
 TAIL = [0, 4366128403083131757, 13582886257094398792, 4365834109879625876, 4360414030434708406, 4361066948569222253, 4356828907110576048, 4364097860734309385, 13588402342996091432, 13581505024848930077, 4363345029737015988, 4355455812241575463, 4362891239881388935, 4355946959017544883, 4356286533989107623, 13587350259894555120]
@@ -17,6 +21,9 @@ _SRC = r"""
 #include <fenv.h>
 #include <stdint.h>
 #include <string.h>
+#include "exp_rare.h"
+double RARE_T = 0x1.61da04cbafe44p+9;   /* 1021 ln2, as exp_np.cuh */
+void set_rare(double t) { RARE_T = t; }
 static const uint64_t TOP[16] = {%s};
 static const uint64_t TAIL[16] = {%s};
 static double d(uint64_t u) { double x; memcpy(&x, &u, 8); return x; }
@@ -31,6 +38,7 @@ double exp_np(double x) {
   if (x != x) return x;
   if (x > 709.782712893384) return INFINITY;
   if (x < -745.1332191019412) return 0.0;
+  if (fabs(x) >= RARE_T) return gevo_exp_rare(x);
   fesetround(FE_TOWARDZERO);
   double t = fma(x, d(%sULL), d(%sULL));
   fesetround(FE_TONEAREST);
@@ -65,7 +73,7 @@ def _build():
     d = tempfile.mkdtemp()
     c, so = os.path.join(d, "e.c"), os.path.join(d, "e.so")
     open(c, "w").write(src)
-    subprocess.check_call(["gcc", "-O1", "-frounding-math", "-ffp-contract=off",
+    subprocess.check_call(["gcc", "-O1", "-frounding-math", "-ffp-contract=off", "-I", CSRC,
                            "-shared", "-fPIC", c, "-o", so, "-lm"])
     _lib = ctypes.CDLL(so)
     return _lib
