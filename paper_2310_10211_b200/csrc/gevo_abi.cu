@@ -51,6 +51,18 @@ struct DevBuf {
   }
 };
 
+// The DOT arithmetic (GEVO_B200_DTYPE): "f64" (default) -- float64 in the
+// reference's summation orders on DMMA, bit-exact; "tf32" -- tcgen05 tensor
+// cores with tf32 operands and fp32 accumulation (dot_tc.cuh), a
+// reduced-precision mode whose fitness is reported against the reference,
+// not gated.  -1: unknown value.
+int tc_mode() {
+  const char* v = getenv("GEVO_B200_DTYPE");
+  if (!v || !*v || !strcmp(v, "f64")) return 0;
+  if (!strcmp(v, "tf32")) return 1;
+  return -1;
+}
+
 }  // namespace
 
 struct gevo_ctx {
@@ -479,6 +491,8 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   a.results = static_cast<gevo_result*>(ctx->results.p);
   a.final_weights = final_weights ? static_cast<double*>(ctx->finalw.p) : nullptr;
   a.smem_elems = h->max_smem;
+  a.tc = tc_mode();
+  if (a.tc < 0) return fail(ctx, GEVO_E_ARG, "GEVO_B200_DTYPE must be f64 or tf32");
   a.prof = nullptr;
   if (ctx->profile) {
     if (ctx->prof.ensure(GEVO_PROFILE_SLOTS * 2 * 8, ctx->stream)) return fail(ctx, GEVO_E_CUDA, "profile alloc");
@@ -563,6 +577,8 @@ int gevo_exec_once(gevo_ctx* ctx, const void* plan, size_t plan_bytes, const dou
   a.arena = static_cast<double*>(ctx->arena.p);
   a.params = static_cast<const double*>(ctx->params.p);
   a.outs = static_cast<double*>(ctx->outs.p);
+  a.tc = tc_mode();
+  if (a.tc < 0) return fail(ctx, GEVO_E_ARG, "GEVO_B200_DTYPE must be f64 or tf32");
   a.smem_elems = h->max_smem;
   launch_once(a, h->n_prog, ctx->stream);
   CK(cudaGetLastError());

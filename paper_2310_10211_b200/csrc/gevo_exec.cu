@@ -41,11 +41,23 @@ struct EpiDev {
   int64_t st0[kEpiExt], st1[kEpiExt];
 };
 
+// tensor-core (tcgen05, tf32 mode) state of a CTA: TMEM columns and the
+// two staging mbarriers (dot_tc.cuh)
+struct TcState {
+  uint32_t tmem;
+  uint32_t ph;                        // bit b: parity of the next wait on stage b
+  uint32_t pending;                   // bit b: a commit on stage b not yet waited for
+  __align__(8) uint64_t mbar[2];
+};
+
 struct Shared {
   double* base[GEVO_NBUF];
   int flag;
   int wrong;
   EpiDev epi;
+  int tc_on;                          // DOTs on tcgen05 (GEVO_B200_DTYPE=tf32)
+  TcState tc;
+  unsigned long long* prof;           // nullable: profile counters (dot_tc phases)
 };
 
 __device__ __forceinline__ double* opptr(const Shared& S, const gevo_operand& o) {
@@ -729,6 +741,7 @@ __device__ __noinline__ void run_ew_chain(Shared& S, const gevo_instr& I) {
 
 }  // namespace gevo
 #include "dot_staged.cuh"
+#include "dot_tc.cuh"
 namespace gevo {
 
 __device__ __noinline__ void run_dot(Shared& S, const gevo_instr& I, double* stage) {
@@ -755,6 +768,10 @@ __device__ __noinline__ void run_dot(Shared& S, const gevo_instr& I, double* sta
   d.K = I.aux[0];
   const int N = I.shp[1];
   const bool integer = I.kin != GEVO_K_F64;
+  if (S.tc_on && !integer) {          // reduced-precision mode: every f64 dot on tcgen05
+    dot_tc(S.tc, d, 0, N, epi, stage, S.prof);
+    return;
+  }
   const int split = integer ? N : min(I.aux[1], N);
   d.xrow = 1 << 30;
   dot_columns(d, 0, split, I.sub, integer, stage, epi);
@@ -980,6 +997,12 @@ eval_kernel(EvalArgs args) {
   double* dstage = dyn_smem;                // dot staging tiles
   double* smem_arena = dyn_smem + kStageElems;
   const gevo_prog P = args.progs[blockIdx.x];
+  if (threadIdx.x == 0) {
+    S.tc_on = args.tc;
+    S.prof = args.prof;
+  }
+  __syncthreads();
+  if (args.tc) tc_setup(S.tc);
 #ifdef GEVO_DOT_TIMING
   if (threadIdx.x == 0) g_dot_prof = args.prof;
 #endif
@@ -1130,6 +1153,7 @@ eval_kernel(EvalArgs args) {
       for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) dst[i] = b[i];
     }
   }
+  if (args.tc) tc_teardown(S.tc);
 }
 
 // run one function once per prog with explicit params (tests, tools)
@@ -1142,6 +1166,8 @@ exec_once_kernel(OnceArgs args) {
   double* smem_arena = dyn_smem + kStageElems;
   const gevo_prog P = args.progs[blockIdx.x];
   if (threadIdx.x == 0) {
+    S.tc_on = args.tc;
+    S.prof = nullptr;
     S.base[GEVO_BUF_ARENA] = args.arena + P.arena_off;
     S.base[GEVO_BUF_SMEM] = smem_arena;
     S.base[GEVO_BUF_CONST] = const_cast<double*>(args.consts) + P.const_off;
@@ -1151,8 +1177,10 @@ exec_once_kernel(OnceArgs args) {
     }
   }
   __syncthreads();
+  if (args.tc) tc_setup(S.tc);
   const gevo_instr* ins = stage(cache, args.instrs + P.train0, P.train0_n);
   run_instrs(S, ins, P.train0_n, dstage, nullptr);
+  if (args.tc) tc_teardown(S.tc);
 }
 
 // The dynamic shared-memory ceiling is a per-function attribute shared by

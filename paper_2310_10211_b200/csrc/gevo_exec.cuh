@@ -26,6 +26,7 @@ struct EvalArgs {
   double* final_weights;      // nullable
   int smem_elems;             // shared-memory scratch tier per CTA
   unsigned long long* prof;   // nullable: per-instruction-class cycles
+  int tc;                     // 1: DOTs on tcgen05 in tf32 (GEVO_B200_DTYPE=tf32)
 };
 
 struct OnceArgs {
@@ -36,6 +37,7 @@ struct OnceArgs {
   const double* params;
   double* outs;
   int smem_elems;
+  int tc;                     // as EvalArgs::tc
 };
 
 void launch_eval(const EvalArgs& a, int n_prog, cudaStream_t st);

@@ -22,11 +22,19 @@ def main(n=256):
     ev.evaluate_variants(fns)
     ms = ev.ctx.last_kernel_ms()
     prof = ev.ctx.profile(False)
+    tc = {k: v for k, v in prof.items() if k[0] == 7}      # dot_tc phases (slots 240..)
+    prof = {k: v for k, v in prof.items() if k[0] != 7}
     tot = sum(c for c, _ in prof.values())
     print(f"kernel {ms:.1f} ms; CTA-cycles profiled {tot:.3e}")
     for (op, sub, big), (cyc, cnt) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
         print(f"{OPS.get(op, op):7s} sub={sub:2d} {'big' if big else 'small':5s} "
               f"{100 * cyc / tot:5.1f}%  count={cnt:9d}  cycles/instr={cyc / cnt:9.0f}")
+    names = ["wait for a stage", "stage (loads, tf32, stores) + fence + barrier", "MMA issue + commit",
+             "wait for the accumulator", "TMEM read + epilogue"]
+    for (op, sub, big), (cyc, cnt) in sorted(tc.items()):
+        ph = 2 * (sub - 8) + big
+        print(f"tcgen05 phase {ph} {names[ph] if ph < len(names) else ''}: {100 * cyc / tot:5.1f}% of CTA cycles, "
+              f"count={cnt}, cycles each={cyc / cnt:8.0f}")
 
 
 if __name__ == "__main__":
