@@ -54,6 +54,7 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-cnn", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-tf32", action="store_true", help="skip the tf32 (tcgen05) side line")
     return p.parse_args()
 
 
@@ -378,6 +379,38 @@ def main():
             kern_ms.append(ev.ctx.last_kernel_ms())
             alg_bytes.append(sum(per_individual_bytes(f, steps_cfg, nb) for f in fns))
             alg_flops.append(sum(per_individual_flops(f, steps_cfg, nb) for f in fns))
+    # (1b) the reduced-precision mode on the same plans: every f64 DOT on
+    # tcgen05 (GEVO_B200_DTYPE=tf32); device time and the error's exact-match
+    # rate against the reference -- a side line, never the headline (the
+    # reference computes in float64)
+    tf32 = None
+    if not args.no_tf32:
+        t_ms, t_exact, t_n = [], 0, 0
+        os.environ["GEVO_B200_DTYPE"] = "tf32"
+        try:
+            for s in range(args.warmup, total_steps):
+                fns, vps = shard_steps[s]
+                p = build_population_plan(vps, ev.weight_shapes, ev.batch * ev.classes)
+                flush.zero_()
+                barrier()
+                res, _ = ev.ctx.eval(p.blob, p.n_prog, 0, steps_cfg, wl.config.finite_check_every, 0, 0,
+                                     ev.weight_elems, False)
+                t_ms.append(ev.ctx.last_kernel_ms())
+                mine = pops[s][rank::world]
+                if len(mine) != len(vps):
+                    continue
+                for k, ind in enumerate(mine):
+                    err = 1.0 if res["status"][k] != 0 else int(res["wrong"][k]) / int(res["total"][k])
+                    t_n += 1
+                    t_exact += err == ind["error"]
+        finally:
+            del os.environ["GEVO_B200_DTYPE"]
+        tf32 = {"value": len(pops[0][rank::world]) * len(t_ms) / (sum(t_ms) / 1e3), "unit": UNIT,
+                "ms_per_step": statistics.mean(t_ms), "dtype": "tf32 (tcgen05.mma kind::tf32, fp32 "
+                "accumulation; every other op float64)",
+                "error_exact_vs_reference": {"exact": t_exact, "of": t_n},
+                "tolerance": "per dot |err| <= 2e-3 * sum|a||b|; one train_step within 2e-3 normwise "
+                             "(tests/test_tc.py)"}
     # (2) e2e through the reference's seam: _Evaluator(workload)(patches)
     wall_s, h2d, d2h, e2e_launches = [], [], [], 0
     parity_ok = parity_n = 0
@@ -478,6 +511,8 @@ def main():
         }
         if cnn_line is not None:
             line["cnn"] = cnn_line
+        if tf32 is not None:
+            line["tf32"] = tf32
         print(json.dumps(line), flush=True)
     ev.close()
     if world > 1:

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libgevo.so")
-SOURCES = ["gevo_exec.cu", "nsga2.cu", "splits.cu", "gevo_abi.cu"]
+SOURCES = ["gevo_exec.cu", "gevo_exec_tc.cu", "nsga2.cu", "splits.cu", "gevo_abi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -33,21 +33,37 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> str:
+    """Compile every source to an object in parallel (the two executor
+    builds dominate: ~2.5 min each), then link libgevo.so."""
     out = out or LIB
     if not force and out == LIB and not needs_build():
         return LIB
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
-           "-Xcompiler", "-fPIC", "-shared", "-I", INCLUDE, "-I", CSRC,
-           *[f"-D{d}" for d in defines], "-o", out + ".tmp"]
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
+             "-I", INCLUDE, "-I", CSRC, *[f"-D{d}" for d in defines]]
     if verbose:
-        cmd += ["-Xptxas", "-v"]
-    cmd += [os.path.join(CSRC, s) for s in SOURCES] + ["-ldl"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libgevo.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        flags += ["-Xptxas", "-v"]
+    with tempfile.TemporaryDirectory() as tmp:
+        objs = [os.path.join(tmp, s.replace(".cu", ".o")) for s in SOURCES]
+
+        def compile_one(src_obj):
+            src, obj = src_obj
+            return subprocess.run([NVCC, *flags, "-c", os.path.join(CSRC, src), "-o", obj],
+                                  capture_output=True, text=True)
+        with ThreadPoolExecutor(len(SOURCES)) as pool:
+            results = list(pool.map(compile_one, zip(SOURCES, objs)))
+        for res in results:
+            if verbose:
+                sys.stderr.write(res.stderr)
+            if res.returncode != 0:
+                sys.stderr.write(res.stdout + res.stderr)
+                raise RuntimeError("nvcc failed building libgevo.so")
+        res = subprocess.run([NVCC, *ARCH, "-shared", "-o", out + ".tmp", *objs, "-ldl"],
+                             capture_output=True, text=True)
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("nvcc failed linking libgevo.so")
     os.replace(out + ".tmp", out)
     return out
 

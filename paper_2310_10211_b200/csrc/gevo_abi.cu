@@ -51,6 +51,10 @@ struct DevBuf {
   }
 };
 
+// the tf32 executor build (gevo_exec_tc.cu, its own module)
+extern "C" void gevo_internal_launch_eval_tc(const void* a, int n_prog, cudaStream_t st);
+extern "C" void gevo_internal_launch_once_tc(const void* a, int n_prog, cudaStream_t st);
+
 // The DOT arithmetic (GEVO_B200_DTYPE): "f64" (default) -- float64 in the
 // reference's summation orders on DMMA, bit-exact; "tf32" -- tcgen05 tensor
 // cores with tf32 operands and fp32 accumulation (dot_tc.cuh), a
@@ -502,7 +506,8 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   if (a.mode == GEVO_MODE_TRAIN && a.train_nb == 0 && a.steps > 0)
     return fail(ctx, GEVO_E_ARG, "train split has no whole batch");
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
-  launch_eval(a, h->n_prog, ctx->stream);
+  if (a.tc) gevo_internal_launch_eval_tc(&a, h->n_prog, ctx->stream);
+  else launch_eval(a, h->n_prog, ctx->stream);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev1, ctx->stream));
   std::vector<gevo_result> per_prog((size_t)h->n_prog);
@@ -580,7 +585,8 @@ int gevo_exec_once(gevo_ctx* ctx, const void* plan, size_t plan_bytes, const dou
   a.tc = tc_mode();
   if (a.tc < 0) return fail(ctx, GEVO_E_ARG, "GEVO_B200_DTYPE must be f64 or tf32");
   a.smem_elems = h->max_smem;
-  launch_once(a, h->n_prog, ctx->stream);
+  if (a.tc) gevo_internal_launch_once_tc(&a, h->n_prog, ctx->stream);
+  else launch_once(a, h->n_prog, ctx->stream);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(outs, ctx->outs.p, out_words * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));

@@ -12,6 +12,21 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <mutex>
+// This file is compiled twice (build.py): GEVO_TC_MODE 0 is the float64
+// parity executor; GEVO_TC_MODE 1 (gevo_exec_tc.cu) is the same executor
+// with every f64 DOT on tcgen05 (dot_tc.cuh), as separate kernels and
+// launchers (`*_tc`).  Keeping the tensor-core path out of the float64
+// build keeps its register allocation: adding the dot_tc call to the one
+// kernel raised the spills of every DMMA dot path and cost ~30 % of the
+// parity mode's speed (measured).
+#ifndef GEVO_TC_MODE
+#define GEVO_TC_MODE 0
+#endif
+#if GEVO_TC_MODE
+#define GEVO_KNAME(x) x##_tc
+#else
+#define GEVO_KNAME(x) x
+#endif
 #include "gevo_plan.h"
 #include "exec_core.cuh"
 #include "exp_np.cuh"
@@ -741,7 +756,9 @@ __device__ __noinline__ void run_ew_chain(Shared& S, const gevo_instr& I) {
 
 }  // namespace gevo
 #include "dot_staged.cuh"
+#if GEVO_TC_MODE
 #include "dot_tc.cuh"
+#endif
 namespace gevo {
 
 __device__ __noinline__ void run_dot(Shared& S, const gevo_instr& I, double* stage) {
@@ -768,10 +785,12 @@ __device__ __noinline__ void run_dot(Shared& S, const gevo_instr& I, double* sta
   d.K = I.aux[0];
   const int N = I.shp[1];
   const bool integer = I.kin != GEVO_K_F64;
-  if (S.tc_on && !integer) {          // reduced-precision mode: every f64 dot on tcgen05
+#if GEVO_TC_MODE
+  if (!integer) {                     // reduced-precision mode: every f64 dot on tcgen05
     dot_tc(S.tc, d, 0, N, epi, stage, S.prof);
     return;
   }
+#endif
   const int split = integer ? N : min(I.aux[1], N);
   d.xrow = 1 << 30;
   dot_columns(d, 0, split, I.sub, integer, stage, epi);
@@ -990,7 +1009,7 @@ __device__ bool all_finite(const double* w, int n) {
 }
 
 __global__ void __launch_bounds__(kThreads, GEVO_MIN_BLOCKS)
-eval_kernel(EvalArgs args) {
+GEVO_KNAME(eval_kernel)(EvalArgs args) {
   __shared__ Shared S;
   __shared__ gevo_instr cache[kInstrCache];
   extern __shared__ double dyn_smem[];
@@ -998,11 +1017,13 @@ eval_kernel(EvalArgs args) {
   double* smem_arena = dyn_smem + kStageElems;
   const gevo_prog P = args.progs[blockIdx.x];
   if (threadIdx.x == 0) {
-    S.tc_on = args.tc;
+    S.tc_on = GEVO_TC_MODE;
     S.prof = args.prof;
   }
   __syncthreads();
-  if (args.tc) tc_setup(S.tc);
+#if GEVO_TC_MODE
+  tc_setup(S.tc);
+#endif
 #ifdef GEVO_DOT_TIMING
   if (threadIdx.x == 0) g_dot_prof = args.prof;
 #endif
@@ -1153,12 +1174,14 @@ eval_kernel(EvalArgs args) {
       for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) dst[i] = b[i];
     }
   }
-  if (args.tc) tc_teardown(S.tc);
+#if GEVO_TC_MODE
+  tc_teardown(S.tc);
+#endif
 }
 
 // run one function once per prog with explicit params (tests, tools)
 __global__ void __launch_bounds__(kThreads, GEVO_MIN_BLOCKS)
-exec_once_kernel(OnceArgs args) {
+GEVO_KNAME(exec_once_kernel)(OnceArgs args) {
   __shared__ Shared S;
   __shared__ gevo_instr cache[kInstrCache];
   extern __shared__ double dyn_smem[];
@@ -1166,7 +1189,7 @@ exec_once_kernel(OnceArgs args) {
   double* smem_arena = dyn_smem + kStageElems;
   const gevo_prog P = args.progs[blockIdx.x];
   if (threadIdx.x == 0) {
-    S.tc_on = args.tc;
+    S.tc_on = GEVO_TC_MODE;
     S.prof = nullptr;
     S.base[GEVO_BUF_ARENA] = args.arena + P.arena_off;
     S.base[GEVO_BUF_SMEM] = smem_arena;
@@ -1177,10 +1200,14 @@ exec_once_kernel(OnceArgs args) {
     }
   }
   __syncthreads();
-  if (args.tc) tc_setup(S.tc);
+#if GEVO_TC_MODE
+  tc_setup(S.tc);
+#endif
   const gevo_instr* ins = stage(cache, args.instrs + P.train0, P.train0_n);
   run_instrs(S, ins, P.train0_n, dstage, nullptr);
-  if (args.tc) tc_teardown(S.tc);
+#if GEVO_TC_MODE
+  tc_teardown(S.tc);
+#endif
 }
 
 // The dynamic shared-memory ceiling is a per-function attribute shared by
@@ -1201,16 +1228,16 @@ static void raise_smem_ceiling(K kernel) {
   });
 }
 
-void launch_eval(const EvalArgs& a, int n_prog, cudaStream_t st) {
+void GEVO_KNAME(launch_eval)(const EvalArgs& a, int n_prog, cudaStream_t st) {
   const size_t smem = (size_t)(a.smem_elems + kStageElems) * sizeof(double);
-  raise_smem_ceiling(eval_kernel);
-  eval_kernel<<<n_prog, kThreads, smem, st>>>(a);
+  raise_smem_ceiling(GEVO_KNAME(eval_kernel));
+  GEVO_KNAME(eval_kernel)<<<n_prog, kThreads, smem, st>>>(a);
 }
 
-void launch_once(const OnceArgs& a, int n_prog, cudaStream_t st) {
+void GEVO_KNAME(launch_once)(const OnceArgs& a, int n_prog, cudaStream_t st) {
   const size_t smem = (size_t)(a.smem_elems + kStageElems) * sizeof(double);
-  raise_smem_ceiling(exec_once_kernel);
-  exec_once_kernel<<<n_prog, kThreads, smem, st>>>(a);
+  raise_smem_ceiling(GEVO_KNAME(exec_once_kernel));
+  GEVO_KNAME(exec_once_kernel)<<<n_prog, kThreads, smem, st>>>(a);
 }
 
 }  // namespace gevo

@@ -42,6 +42,9 @@ struct OnceArgs {
 
 void launch_eval(const EvalArgs& a, int n_prog, cudaStream_t st);
 void launch_once(const OnceArgs& a, int n_prog, cudaStream_t st);
+// (namespace gevo_tc, the tf32 build: gevo_exec_tc.cu wraps these two)
+void launch_eval_tc(const EvalArgs& a, int n_prog, cudaStream_t st);
+void launch_once_tc(const OnceArgs& a, int n_prog, cudaStream_t st);
 
 // NSGA-II (nsga2.cu)
 struct NsArgs {

@@ -147,12 +147,12 @@ def _collect(jobs):
 
 
 def _arena_budget() -> float:
-    """GEVO_B200_ARENA_GB (default 64) in bytes of requested scratch.  The
+    """GEVO_B200_ARENA_GB (default 80: 64 GB of requested scratch) in bytes.  The
     library's buffers grow to request + 25 % (DevBuf::ensure, gevo_abi.cu),
     so the grouping budget is the knob / 1.25: the device footprint stays
     within the figure (approximately: growth briefly holds the old buffer
     too, stream-ordered)."""
-    return float(os.environ.get("GEVO_B200_ARENA_GB", "64")) * 1e9 / 1.25
+    return float(os.environ.get("GEVO_B200_ARENA_GB", "80")) * 1e9 / 1.25
 
 
 def lower_all(variants, cost_table, training, steps=600):
@@ -409,8 +409,8 @@ class DeviceEvaluator:
 
     def _scratch_groups(self, lowered, shares=1):
         """[g0, g1) ranges of `lowered` whose device scratch (arena, probs
-        and weight ping-pong per individual) fits GEVO_B200_ARENA_GB (default
-        64) split over `shares` concurrent launches."""
+        and weight ping-pong per individual) fits the scratch budget
+        (_arena_budget) split over `shares` concurrent launches."""
         budget = _arena_budget() / max(1, shares)
         fixed = 8 * (((self.batch * self.classes + 15) & ~15) + 2 * ((self.weight_elems + 15) & ~15))
         groups, g0, acc = [], 0, 0
@@ -426,7 +426,7 @@ class DeviceEvaluator:
     def score_parts(self, lowered, n_score, n_total=None, shares=1):
         """Programs per prediction-mode individual (plan.build_population_plan
         `parts`): enough to give the launch two CTAs per SM, at most one per
-        scored batch, and within GEVO_B200_ARENA_GB (default 64) of scratch.
+        scored batch, and within GEVO_B200_ARENA_GB (default 80, i.e. 64 GB requested) of scratch.
         `n_total` is the call's individual count when this launch holds one
         half of it (the halves run concurrently).  GEVO_B200_PARTS overrides."""
         n = len(lowered)

@@ -15,7 +15,7 @@ if [ -z "$NO_REF" ]; then
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${TAG}_reference_arm.log 2>&1; tail -n 1 gpurun_out/${TAG}_reference_arm.log
 fi
 if [ -z "$NO_NCU" ]; then
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-cnn --no-e2e > /dev/null 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:eval_kernel -s 1 -c 1 -o gpurun_out/${TAG}_prof python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-cnn --no-e2e > gpurun_out/${TAG}_ncu.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-cnn --no-e2e --no-tf32 > /dev/null 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:eval_kernel -s 1 -c 1 -o gpurun_out/${TAG}_prof python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-cnn --no-e2e --no-tf32 > gpurun_out/${TAG}_ncu.log 2>&1
 tail -n 1 gpurun_out/${TAG}_ncu.log
 fi
