@@ -2,12 +2,15 @@
 
 Workload (BASELINE.json configs[1]): train2fc (784-32-10 MLP, 600 SGD steps
 + 31 scored batches per individual) on synthetic MNIST-shaped data.  A step
-evaluates one population of `--pop` (default 256) fresh mutated individuals,
-drawn from a recorded seeded GA run (pop 256 x 10 generations,
+evaluates one population of `--pop` fresh mutated individuals, drawn from a
+recorded seeded GA run (pop 256 x 10 generations,
 tests/golden/bench_train_pool.json.gz): real patches of the reference's
-genome, not copies of one program.  With N GPUs the same population is
-sharded over the ranks (strong scaling: configs[1] is "population 256 ...
-sharded over 8xB200").
+genome, not copies of one program.  The population is sharded over the N
+ranks; by default it is 256 per GPU (weak scaling: 256, 512, 1024, 2048 at
+N = 1, 2, 4, 8 -- points of configs[4]'s 64-4096 sweep).  With N > 1 the
+line also carries `strong_pop256`: configs[1] itself, population 256
+sharded over the N GPUs (device time; each GPU then holds 256/N
+individuals, which underfill it -- SURVEY.md §7.3 item 8).
 
   value  = individuals / device time of the evaluation kernels (plans
            resident; CUDA events on the launching stream; max over ranks)
@@ -50,7 +53,8 @@ def parse_args():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--pop", type=int, default=POP, help="population per step (whole job)")
+    p.add_argument("--pop", type=int, default=None,
+                   help="population per step, whole job (default 256 per GPU)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-cnn", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -248,7 +252,7 @@ def run_reference(args, world, rank):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * args.pop / value, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "population": args.pop, "sample": sample},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                              "sample": sample},
@@ -321,6 +325,8 @@ def cnn_measure(local, steps=1):
 def main():
     args = parse_args()
     world, rank, local = dist_setup(args)
+    if args.pop is None:
+        args.pop = POP * world
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
@@ -379,6 +385,29 @@ def main():
             kern_ms.append(ev.ctx.last_kernel_ms())
             alg_bytes.append(sum(per_individual_bytes(f, steps_cfg, nb) for f in fns))
             alg_flops.append(sum(per_individual_flops(f, steps_cfg, nb) for f in fns))
+    # (1a) N > 1: configs[1] as written -- population 256 sharded over the N
+    # GPUs (strong scaling), device time, max over ranks
+    strong = None
+    if world > 1:
+        s_ms = []
+        for s in range(args.warmup, total_steps):
+            mine = pops[s][:POP][rank::world]
+            fns = [{n: parse_function(i[n]) for n in ("forward", "train_step")} for i in mine]
+            vps = [v for v in lower_all(fns, wl.config.cost_table, True, steps_cfg) if v is not None]
+            p = build_population_plan(vps, ev.weight_shapes, ev.batch * ev.classes,
+                                      order=sm_aware_order([device_weight(v, steps_cfg, nb) for v in vps],
+                                                           ev.n_sms))
+            flush.zero_()
+            barrier()
+            ev.ctx.eval(p.blob, p.n_prog, 0, steps_cfg, wl.config.finite_check_every, 0, 0,
+                        ev.weight_elems, False)
+            s_ms.append(ev.ctx.last_kernel_ms())
+        import torch.distributed as dist
+        t = torch.tensor([sum(s_ms) / 1e3], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        strong = {"population": POP, "value": POP * len(s_ms) / t.item(), "unit": UNIT,
+                  "ms_per_step": 1e3 * t.item() / len(s_ms), "scaling": "strong",
+                  "note": "configs[1]: population 256 sharded over the GPUs (256/N per GPU)"}
     # (1b) the reduced-precision mode on the same plans: every f64 DOT on
     # tcgen05 (GEVO_B200_DTYPE=tf32); device time and the error's exact-match
     # rate against the reference -- a side line, never the headline (the
@@ -484,7 +513,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * dev_s / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded synthetic_digits, recorded GA patches)",
             "config": {"workload": f"{WORKLOAD}, population {args.pop}",
                        "population": args.pop, "population_per_gpu": args.pop / world,
@@ -513,6 +542,8 @@ def main():
             line["cnn"] = cnn_line
         if tf32 is not None:
             line["tf32"] = tf32
+        if strong is not None:
+            line["strong_pop256"] = strong
         print(json.dumps(line), flush=True)
     ev.close()
     if world > 1:
