@@ -77,6 +77,10 @@ struct gevo_ctx {
   double* weights = nullptr;
   int64_t weight_elems = 0;
   DevBuf plan, arena, results, finalw, params, outs, ns;
+  DevBuf wreg;                       // training: every program's weight blocks (L2 window)
+  void* window_base = nullptr;       // the stream's current L2 access window
+  size_t window_bytes = 0;
+  bool persist_limit_set = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   bool profile = false;
@@ -222,6 +226,7 @@ int gevo_destroy(gevo_ctx* ctx) {
   ctx->outs.release();
   ctx->ns.release();
   ctx->gather.release();
+  ctx->wreg.release();
   gevo_comm_destroy(ctx);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -505,6 +510,48 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   }
   if (a.mode == GEVO_MODE_TRAIN && a.train_nb == 0 && a.steps > 0)
     return fail(ctx, GEVO_E_ARG, "train split has no whole batch");
+  // Training: the weight blocks move to one region, all block 0s first.
+  // Block 0 is where in-place weights live for the whole launch (w1: 200 KB
+  // per individual, read twice and written once per step), so one L2
+  // persisting access window covers exactly the hot weights (GEVO_B200_L2WINDOW=0
+  // turns the window off).  The window stays on the context's stream; the
+  // blocks are zeroed at every launch start, so lines left persisting hold no
+  // input of the next launch.
+  if (a.mode == GEVO_MODE_TRAIN && a.steps > 0) {
+    const size_t wsz = (size_t)((h->weight_elems + 15) & ~15);
+    const size_t bytes = 2 * wsz * (size_t)h->n_prog * sizeof(double);
+    if (ctx->wreg.ensure(bytes, ctx->stream)) return fail(ctx, GEVO_E_CUDA, "weight region alloc failed");
+    a.wreg = static_cast<double*>(ctx->wreg.p);
+    a.n_prog = h->n_prog;
+    const char* ew = getenv("GEVO_B200_L2WINDOW");
+    if (!ew || atoi(ew) != 0) {
+      int max_persist = 0, max_window = 0;
+      cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
+      cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);
+      const size_t hot = wsz * (size_t)h->n_prog * sizeof(double);
+      const size_t nbytes = hot < (size_t)max_window ? hot : (size_t)max_window;
+      if (max_persist > 0 && max_window > 0 &&
+          (ctx->window_base != ctx->wreg.p || ctx->window_bytes != nbytes)) {
+        if (!ctx->persist_limit_set) {      // device-wide, once per context
+          cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+          ctx->persist_limit_set = true;
+        }
+        cudaStreamAttrValue v;
+        memset(&v, 0, sizeof v);
+        v.accessPolicyWindow.base_ptr = ctx->wreg.p;
+        v.accessPolicyWindow.num_bytes = hot < (size_t)max_window ? hot : (size_t)max_window;
+        const double ratio = (double)max_persist / (double)v.accessPolicyWindow.num_bytes;
+        v.accessPolicyWindow.hitRatio = ratio < 1.0 ? (float)ratio : 1.0f;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        if (cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess) {
+          ctx->window_base = ctx->wreg.p;
+          ctx->window_bytes = nbytes;
+        }
+        cudaGetLastError();
+      }
+    }
+  }
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
   if (a.tc) gevo_internal_launch_eval_tc(&a, h->n_prog, ctx->stream);
   else launch_eval(a, h->n_prog, ctx->stream);

@@ -1032,7 +1032,14 @@ GEVO_KNAME(eval_kernel)(EvalArgs args) {
   const int psz = (args.probs_elems + 15) & ~15;
   double* scratch = ind;
   double* probs = ind + P.arena_elems;
+  // weight blocks: in the launch's weight region when the host gave one (all
+  // block 0s contiguous -- the in-place weights' home -- so one L2 persisting
+  // window covers them; gevo_abi.cu), else after the individual's scratch
   double* wbuf[2] = {probs + psz, probs + psz + wsz};
+  if (args.wreg) {
+    wbuf[0] = args.wreg + (int64_t)blockIdx.x * wsz;
+    wbuf[1] = args.wreg + (int64_t)(args.n_prog + blockIdx.x) * wsz;
+  }
   const double* consts = args.consts + P.const_off;
   const int nw = args.n_weights;
   int status = GEVO_STATUS_OK;

@@ -27,6 +27,9 @@ struct EvalArgs {
   int smem_elems;             // shared-memory scratch tier per CTA
   unsigned long long* prof;   // nullable: per-instruction-class cycles
   int tc;                     // 1: DOTs on tcgen05 in tf32 (GEVO_B200_DTYPE=tf32)
+  double* wreg;               // nullable: weight blocks of all programs, block 0 of
+                              // program i at wreg + i*wsz, block 1 at wreg + (n + i)*wsz
+  int n_prog;                 // programs of the launch (wreg's block-1 offset)
 };
 
 struct OnceArgs {
