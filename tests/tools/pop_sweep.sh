@@ -4,7 +4,7 @@
 OUT=${1:-gpurun_out/pop_sweep.jsonl}
 : > $OUT
 for P in 64 128 256 512 1024 2048 4096; do
-  timeout 900 python bench.py --pop $P --steps 3 --warmup 3 --no-cpu-baseline | tail -n 1 >> $OUT
+  timeout 900 python bench.py --pop $P --steps 3 --warmup 3 --no-cpu-baseline --no-cnn --no-tf32 | tail -n 1 >> $OUT
   python - "$OUT" <<'PY'
 import json, sys
 l = json.loads(open(sys.argv[1]).read().splitlines()[-1])
