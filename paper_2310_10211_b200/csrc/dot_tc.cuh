@@ -10,7 +10,11 @@
 // product error; bench.py reports the exact-match rate and the tolerance.
 //
 // Per 128 x 64 output tile (64 fp32 columns of TMEM, allocated once per
-// CTA): K is walked in 32-wide chunks through two shared-memory stages.  The
+// CTA): K is walked in 32-wide chunks through two shared-memory stages.  When
+// A is a 32-row batch of the training split's x -- the operand every
+// individual shares -- its chunks come by TMA from one fp32 mirror of the
+// split (a tensor map per launch, gevo_abi.cu); the CTA's threads stage the
+// rest.  The
 // CTA's threads stage a chunk -- A rows and B columns, f64 -> tf32 -- in the
 // K-major no-swizzle canonical layout (8-row x 16-byte core matrices: LBO =
 // 128 B between the two core matrices of one MMA's K = 8, SBO = 1 KB between
@@ -64,11 +68,15 @@ __device__ __forceinline__ void tc_wait(uint32_t mbar, uint32_t phase) {
 // start, tc_teardown at the end
 __device__ __forceinline__ void tc_setup(TcState& T) {
   if (threadIdx.x == 0) {
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < 2; ++b) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&T.mbar[b])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&T.tbar[b])));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     T.ph = 0;
     T.pending = 0;
+    T.tph = 0;
+    if (T.tmap) asm volatile("prefetch.tensormap [%0];" ::"l"(T.tmap) : "memory");
   }
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
@@ -96,6 +104,15 @@ __device__ __forceinline__ void tc_drain(TcState& T, int b, uint32_t& ph, uint32
   }
 }
 
+// TMA (cp.async.bulk.tensor) of one 8-row x 4-column fp32 box of the
+// mirrored x -- exactly one core matrix of the canonical layout -- into smem
+// `dst`, completing on mbarrier `bar`
+__device__ __forceinline__ void tma_box(uint32_t dst, const void* map, int col, int row, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(map), "r"(col), "r"(row), "r"(bar) : "memory");
+}
+
 // columns [col0, col1) of the DOT, every row, on tcgen05 (tf32 operands, fp32
 // accumulation); the epilogue (if any) is applied in float64.
 // profile mode: thread 0 adds phase cycles to slots 240.. (op class 7 of
@@ -115,7 +132,10 @@ __device__ __noinline__ void dot_tc(TcState& T, const DotArgs& dref, int col0, i
   const DotArgs d = dref;            // registers, not the caller's stack frame
   long long tt = clock64();
   const int M = d.M, K = d.K, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // TMA destinations need 128-byte alignment: round the staging base up
+  // (48 KB of the 63 KB buffer are used, so the slack fits)
   uint8_t* sm = reinterpret_cast<uint8_t*>(stage_buf);
+  sm += (128u - (smem_u32(sm) & 127u)) & 127u;
   // stage b: B tile at b * kTcTileB, A tile at 2 * kTcTileB + b * kTcTileA
   // (48 KB of the 63 KB staging buffer; an A tile's unstaged row groups are
   // read by the MMA and land in TMEM lanes nobody reads)
@@ -143,11 +163,32 @@ __device__ __noinline__ void dot_tc(TcState& T, const DotArgs& dref, int col0, i
       const double* pb = d.B + (int64_t)bk0 * d.sbk + (int64_t)(n0 + bn0) * d.sbn;
       const int64_t sa_u = (int64_t)amd * d.sam + (int64_t)akd * d.sak;
       const int64_t sb_u = (int64_t)bkd * d.sbk + (int64_t)bnd * d.sbn;
-      const int na = a_kfast ? max(0, min(16, (mt - am0 + 7) / 8)) : 16;   // A slots with rows < mt
+      // A from the shared batch x: TMA boxes of its fp32 mirror, one per
+      // core matrix (8 rows x 4 columns), issued by one thread per chunk
+      int trow0 = -1;
+      if (T.tmap && mt == 32 && d.sak == 1 && d.sam == T.tcols && d.A >= T.tx64) {
+        const int64_t off = (d.A + (int64_t)m0 * d.sam) - T.tx64;
+        if (off < T.trows * (int64_t)T.tcols && off % T.tcols == 0 && (off / T.tcols) % 8 == 0 &&
+            off / T.tcols + 32 <= T.trows)
+          trow0 = (int)(off / T.tcols);
+      }
+      const bool tma_a = trow0 >= 0;
+      const int na = tma_a ? 0 : (a_kfast ? max(0, min(16, (mt - am0 + 7) / 8)) : 16);   // A slots, rows < mt
       for (int c = 0; c < nch; ++c) {
         const int b = c & 1, k0 = c * kTcKC;
         tc_drain(T, b, ph, pending);       // the MMAs that read stage b are done
         tc_tick(prof, 0, tt);
+        if (tma_a && tid == 0) {
+          const uint32_t bar = smem_u32(&T.tbar[b]);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(32 * kTcKC * 4)
+                       : "memory");
+          const uint32_t a0 = sbase + 2 * kTcTileB + b * kTcTileA;
+#pragma unroll
+          for (int rg = 0; rg < 4; ++rg)
+#pragma unroll
+            for (int cg = 0; cg < kTcKC / 4; ++cg)
+              tma_box(a0 + rg * kTcSBO + cg * kTcLBO, T.tmap, k0 + cg * 4, trow0 + rg * 8, bar);
+        }
         uint8_t* As = sm + 2 * kTcTileB + b * kTcTileA;
         uint8_t* Bs = sm + b * kTcTileB;
         const double* pac = pa + (int64_t)k0 * d.sak;
@@ -187,6 +228,10 @@ __device__ __noinline__ void dot_tc(TcState& T, const DotArgs& dref, int col0, i
         __syncthreads();
         tc_tick(prof, 1, tt);
         if (tid == 0) {
+          if (tma_a) {                     // the chunk's A boxes have landed
+            tc_wait(smem_u32(&T.tbar[b]), (T.tph >> b) & 1);
+            T.tph ^= 1u << b;
+          }
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a0 = sbase + 2 * kTcTileB + b * kTcTileA, b0 = sbase + b * kTcTileB;
 #pragma unroll

@@ -3,6 +3,8 @@
 // Owns the device, one stream, the resident dataset splits, the shared
 // initial weights and the growable device arena; validates plans; no C++
 // exception crosses the boundary.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -78,6 +80,7 @@ struct gevo_ctx {
   int64_t weight_elems = 0;
   DevBuf plan, arena, results, finalw, params, outs, ns;
   DevBuf wreg;                       // training: every program's weight blocks (L2 window)
+  DevBuf x32;                        // tf32 mode: fp32 mirror of the training split's x
   void* window_base = nullptr;       // the stream's current L2 access window
   size_t window_bytes = 0;
   bool persist_limit_set = false;
@@ -227,6 +230,7 @@ int gevo_destroy(gevo_ctx* ctx) {
   ctx->ns.release();
   ctx->gather.release();
   ctx->wreg.release();
+  ctx->x32.release();
   gevo_comm_destroy(ctx);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -510,6 +514,42 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   }
   if (a.mode == GEVO_MODE_TRAIN && a.train_nb == 0 && a.steps > 0)
     return fail(ctx, GEVO_E_ARG, "train split has no whole batch");
+  // tf32 mode, training: an fp32 mirror of the training split's x and a TMA
+  // tensor map over it (8 x 4 boxes = one canonical core matrix each), so the
+  // tcgen05 dots take their shared A operand by cp.async.bulk.tensor
+  // (dot_tc.cuh).  GEVO_B200_TMA=0 stages it with the threads instead.
+  if (a.tc && a.mode == GEVO_MODE_TRAIN && tr && tr->x && tr->features % 4 == 0) {
+    const char* et = getenv("GEVO_B200_TMA");
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+      cudaGetLastError();
+    }
+    const int64_t rows = (int64_t)tr->nb * tr->batch, cols = tr->features;
+    if ((!et || atoi(et) != 0) && encode && rows > 0) {
+      if (ctx->x32.ensure((size_t)(rows * cols) * sizeof(float), ctx->stream))
+        return fail(ctx, GEVO_E_CUDA, "x32 alloc failed");
+      launch_to_f32(tr->x, rows * cols, static_cast<float*>(ctx->x32.p), device_sms(ctx), ctx->stream);
+      CUtensorMap map;
+      cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+      cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
+      cuuint32_t box[2] = {4, 8};
+      cuuint32_t estr[2] = {1, 1};
+      if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ctx->x32.p, dims, strides, box, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+        static_assert(sizeof(map) == sizeof(a.tma_map), "CUtensorMap size");
+        memcpy(a.tma_map, &map, sizeof map);
+        a.tma_x64 = tr->x;
+        a.tma_rows = rows;
+        a.tma_cols = (int)cols;
+      }
+    }
+  }
   // Training: the weight blocks move to one region, all block 0s first.
   // Block 0 is where in-place weights live for the whole launch (w1: 200 KB
   // per individual, read twice and written once per step), so one L2

@@ -62,7 +62,13 @@ struct TcState {
   uint32_t tmem;
   uint32_t ph;                        // bit b: parity of the next wait on stage b
   uint32_t pending;                   // bit b: a commit on stage b not yet waited for
-  __align__(8) uint64_t mbar[2];
+  uint32_t tph;                       // bit b: parity of the next TMA wait on stage b
+  __align__(8) uint64_t mbar[2];      // MMA commits (stage free again)
+  __align__(8) uint64_t tbar[2];      // TMA transactions (stage's A chunk landed)
+  const void* tmap;                   // the launch's tensor map (param space), or null
+  const double* tx64;                 // the f64 x it mirrors
+  int64_t trows;
+  int tcols;
 };
 
 struct Shared {
@@ -1009,7 +1015,7 @@ __device__ bool all_finite(const double* w, int n) {
 }
 
 __global__ void __launch_bounds__(kThreads, GEVO_MIN_BLOCKS)
-GEVO_KNAME(eval_kernel)(EvalArgs args) {
+GEVO_KNAME(eval_kernel)(const __grid_constant__ EvalArgs args) {
   __shared__ Shared S;
   __shared__ gevo_instr cache[kInstrCache];
   extern __shared__ double dyn_smem[];
@@ -1019,6 +1025,10 @@ GEVO_KNAME(eval_kernel)(EvalArgs args) {
   if (threadIdx.x == 0) {
     S.tc_on = GEVO_TC_MODE;
     S.prof = args.prof;
+    S.tc.tmap = args.tma_x64 ? static_cast<const void*>(args.tma_map) : nullptr;
+    S.tc.tx64 = args.tma_x64;
+    S.tc.trows = args.tma_rows;
+    S.tc.tcols = args.tma_cols;
   }
   __syncthreads();
 #if GEVO_TC_MODE
@@ -1208,6 +1218,7 @@ GEVO_KNAME(exec_once_kernel)(OnceArgs args) {
   }
   __syncthreads();
 #if GEVO_TC_MODE
+  if (threadIdx.x == 0) S.tc.tmap = nullptr;
   tc_setup(S.tc);
 #endif
   const gevo_instr* ins = stage(cache, args.instrs + P.train0, P.train0_n);

@@ -30,6 +30,13 @@ struct EvalArgs {
   double* wreg;               // nullable: weight blocks of all programs, block 0 of
                               // program i at wreg + i*wsz, block 1 at wreg + (n + i)*wsz
   int n_prog;                 // programs of the launch (wreg's block-1 offset)
+  // tf32 mode: the training split's x as fp32 under a TMA tensor map; a dot
+  // whose A operand is a batch of that x (row-major, 32 rows) has its A
+  // chunks loaded by cp.async.bulk.tensor instead of the CTA's threads
+  const double* tma_x64;      // nullable: the f64 x the map mirrors
+  int64_t tma_rows;
+  int tma_cols;
+  alignas(64) unsigned char tma_map[128];   // CUtensorMap (opaque)
 };
 
 struct OnceArgs {
@@ -94,6 +101,7 @@ void launch_archive_merge(const ArchArgs& a, cudaStream_t st);
 
 // dataset bytes -> split arrays (splits.cu)
 void launch_decode_u8(const uint8_t* px, int64_t count, double* x, int sms, cudaStream_t st);
+void launch_to_f32(const double* x, int64_t n, float* y, int sms, cudaStream_t st);
 void launch_decode_cifar(const uint8_t* rec, int64_t rows, int C, int HW, double* x,
                          int64_t* labels, int sms, cudaStream_t st);
 void launch_one_hot(const int64_t* labels, int64_t rows, int classes, double* y, int sms,

@@ -80,6 +80,23 @@ static int grid_for(int64_t work, int sms) {
   return (int)(want < 1 ? 1 : (want < cap ? want : cap));
 }
 
+// the tf32 mode's copy of a split's x (the operand TMA feeds to tcgen05):
+// each value rounded to tf32 exactly as the CTA-staged operands are
+// (cvt.rna of the fp32 value), stored as fp32 bits with the low 13 zero
+__global__ void __launch_bounds__(256) to_f32_kernel(const double* __restrict__ x, int64_t n,
+                                                     float* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t t;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"((float)x[i]));
+    y[i] = __uint_as_float(t);
+  }
+}
+
+void launch_to_f32(const double* x, int64_t n, float* y, int sms, cudaStream_t st) {
+  if (n <= 0) return;
+  to_f32_kernel<<<grid_for(n, sms), 256, 0, st>>>(x, n, y);
+}
+
 void launch_decode_u8(const uint8_t* px, int64_t count, double* x, int sms, cudaStream_t st) {
   if (count <= 0) return;
   decode_u8_kernel<<<grid_for((count + 3) / 4, sms), 256, 0, st>>>(px, count, x);
