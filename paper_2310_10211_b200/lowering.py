@@ -39,7 +39,7 @@ BUF_SMEM = 2 + 2 * MAXP
 # SMEM_VALUE_MAX elements are placed there while the per-function total
 # stays within SMEM_BUDGET; everything else goes to the HBM arena.
 SMEM_VALUE_MAX = 4096
-SMEM_BUDGET = 3968
+SMEM_BUDGET = int(os.environ.get("GEVO_B200_SMEM_BUDGET", 3968))
 K_F64, K_I64, K_I1 = 0, 1, 2
 KIND = {"f32": K_F64, "i32": K_I64, "i1": K_I1}
 OP_UNARY, OP_BINARY, OP_SELECT, OP_REDUCE, OP_DOT, OP_PAD, OP_EXT = 1, 2, 3, 4, 5, 6, 7
