@@ -213,7 +213,7 @@ class DeviceEvaluator:
         self.ctx.upload_weights(np.concatenate([a.reshape(-1) for a in w]))
         self.weight_elems = int(sum(a.size for a in w))
         self._flat_weights = np.concatenate([a.reshape(-1) for a in w])
-        self._ctx2 = None
+        self._extra = {}           # chunk k >= 1 -> its own context (_context)
         self._sm_layout = {}
         self.last_timing = {}
         self.last_plan_bytes = 0
@@ -229,19 +229,22 @@ class DeviceEvaluator:
             groups.setdefault(s, []).append(block)
         self._sm_layout[len(order)] = list(groups.values())
 
-    def _second_context(self):
-        """A second context (own stream and buffers) on the same device: the
-        first half of a generation runs on one while the host lowers the
-        second half for the other."""
-        if self._ctx2 is None:
+    def _context(self, k):
+        """Context of chunk k of a generation: chunk 0 uses the evaluator's
+        own; chunk k >= 1 gets a context of its own (stream and buffers) on
+        the same device, so chunk k runs on the device while the host still
+        lowers chunk k + 1."""
+        if k == 0:
+            return self.ctx
+        if k not in self._extra:
             c = _lib.Context(self.device)
             ds, cfg = self.workload.dataset, self.workload.config
             upload_split(c, SPLIT_SEARCH, ds.search, cfg.classes, cfg.batch_size)
             if self._holdout_batches is not None:
                 upload_split(c, SPLIT_HOLDOUT, ds.holdout, cfg.classes, cfg.batch_size)
             c.upload_weights(self._flat_weights)
-            self._ctx2 = c
-        return self._ctx2
+            self._extra[k] = c
+        return self._extra[k]
 
     def _ensure_holdout(self):
         if self._holdout_batches is None:
@@ -249,9 +252,8 @@ class DeviceEvaluator:
             # holdout.reads is bumped by the holdout_report seam, once per
             # report like the reference (fitness.py:407); the upload is not a
             # report
-            for c in (self.ctx, self._ctx2):
-                if c is not None:
-                    upload_split(c, SPLIT_HOLDOUT, ds.holdout, cfg.classes, cfg.batch_size)
+            for c in [self.ctx] + list(self._extra.values()):
+                upload_split(c, SPLIT_HOLDOUT, ds.holdout, cfg.classes, cfg.batch_size)
             self._holdout_batches = len(ds.holdout.labels) // cfg.batch_size
         return self._holdout_batches
 
@@ -289,16 +291,21 @@ class DeviceEvaluator:
         records = np.zeros(len(variants), dtype=_lib.RESULT_DTYPE)
         finals = [None] * len(variants) if want_weights else None
         split = SPLIT_HOLDOUT if holdout else SPLIT_SEARCH
-        # two halves when the pool is used: half A runs on the device (ctypes
-        # releases the GIL) while half B is still being lowered
+        # chunks when the pool is used (GEVO_B200_CHUNKS, default 2): chunk k
+        # runs on the device (ctypes releases the GIL) while chunk k + 1 is
+        # still being lowered
         halves = [idx]
-        if len(idx) >= 2 * POOL_MIN and _lower_pool(_patches[0] if _patches else None) is not None \
-                and os.environ.get("GEVO_B200_HALVES", "1") != "0":
-            halves = [idx[:len(idx) // 2], idx[len(idx) // 2:]]
+        n_chunks = int(os.environ.get("GEVO_B200_CHUNKS", "2"))
+        if os.environ.get("GEVO_B200_HALVES", "1") == "0":
+            n_chunks = 1
+        n_chunks = max(1, min(n_chunks, len(idx) // POOL_MIN))
+        if n_chunks > 1 and _lower_pool(_patches[0] if _patches else None) is not None:
+            bounds = [len(idx) * k // n_chunks for k in range(n_chunks + 1)]
+            halves = [idx[bounds[k]:bounds[k + 1]] for k in range(n_chunks)]
         jobs = [_submit_lowering(variants, h, cfg.cost_table, training, cfg.steps, _patches)
                 for h in halves]
-        ctxs = [self.ctx, self._second_context() if len(halves) > 1 else None]
-        runner, box, launches, failed = None, {}, {}, {}
+        ctxs = [self._context(k) for k in range(len(halves))]
+        runners, box, launches, failed = [], {}, {}, {}
         t_lower = t_pack = 0.0
         plan_bytes = 0
         for h, job in enumerate(jobs):
@@ -357,12 +364,12 @@ class DeviceEvaluator:
                     failed[key] = e
             if h + 1 < len(jobs):
                 import threading
-                runner = threading.Thread(target=run)
-                runner.start()
+                runners.append(threading.Thread(target=run))
+                runners[-1].start()
             else:
                 run()
-        if runner is not None:
-            runner.join()
+        for r in runners:
+            r.join()
         if failed:
             # a device failure in either half is loud, never a missing fitness
             raise failed[min(failed)]
@@ -372,8 +379,8 @@ class DeviceEvaluator:
             # consecutive launches (scratch budget): kernel time summed per
             # half; the halves run concurrently
             self.last_device_ms = max(launches[k][1] for k in used)
-        elif len(used) == 2:
-            self.last_device_ms = _lib.span_ms(ctxs[0], ctxs[1])
+        elif len(used) >= 2:
+            self.last_device_ms = max(_lib.span_ms(ctxs[used[0]], ctxs[k]) for k in used[1:])
         elif used:
             self.last_device_ms = ctxs[used[0]].last_kernel_ms()
         for key in used:
@@ -462,8 +469,9 @@ class DeviceEvaluator:
 
     def close(self):
         self.ctx.close()
-        if self._ctx2 is not None:
-            self._ctx2.close()
+        for c in self._extra.values():
+            c.close()
+        self._extra = {}
 
 
 def baseline_functions(workload: Workload) -> dict:
