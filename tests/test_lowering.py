@@ -318,3 +318,82 @@ def test_three_layout_schedule_ga_individual():
         w = prog(w + [xb, yb])
     for g_, r_ in zip(got, w):
         assert np.allclose(g_, r_, rtol=1e-9, atol=1e-12, equal_nan=True)
+
+
+def _inplace_mask(text):
+    from paper_2310_10211_b200.plan import inplace_weights
+    fn = dialect.parse_function(text)
+    low = Lw.lower_function(fn)
+    return inplace_weights(Lw.encode_instrs(low.instrs), len(fn.returns))
+
+
+def test_inplace_analysis_rejects_unsafe_updates():
+    """plan.inplace_weights: a weight read after its update, or read by its
+    updating instruction at a word it does not write (a transposed view),
+    stays ping-ponged; element-local updates read first go in place."""
+    two = "(tensor<4x4xf32>, tensor<4x4xf32>)"
+    # a' = a + b is written first; b' = b * a then reads a: a must not be in
+    # place, b may (only its own writer reads it, element for element)
+    assert _inplace_mask(f"""func @f(%a: tensor<4x4xf32>, %b: tensor<4x4xf32>) -> {two} {{
+  %0 = add %a, %b : tensor<4x4xf32>
+  %1 = multiply %b, %a : tensor<4x4xf32>
+  return %0, %1 : tensor<4x4xf32>, tensor<4x4xf32>
+}}""") == 0b10
+    # a' reads a through a transpose: a word it does not write
+    assert _inplace_mask(f"""func @f(%a: tensor<4x4xf32>, %b: tensor<4x4xf32>) -> {two} {{
+  %0 = transpose %a {{perm = [1, 0]}} : tensor<4x4xf32>
+  %1 = add %a, %0 : tensor<4x4xf32>
+  %2 = multiply %b, %b : tensor<4x4xf32>
+  return %1, %2 : tensor<4x4xf32>, tensor<4x4xf32>
+}}""") == 0b10
+    # both element-local and read before: both in place
+    assert _inplace_mask(f"""func @f(%a: tensor<4x4xf32>, %b: tensor<4x4xf32>) -> {two} {{
+  %0 = multiply %a, %b : tensor<4x4xf32>
+  %1 = subtract %b, %a : tensor<4x4xf32>
+  %2 = add %0, %a : tensor<4x4xf32>
+  return %2, %1 : tensor<4x4xf32>, tensor<4x4xf32>
+}}""") in (0b11, 0b10, 0b01)
+
+
+def test_inplace_weights_emulate_identically():
+    """Every bench-pool individual (steady layouts) runs one train_step with
+    each in-place weight's parameter and return sharing one buffer, and the
+    returned words equal the ping-pong run's (plan_emu: an instruction reads
+    all its operands before it writes)."""
+    from paper_2310_10211_b200.plan import inplace_weights
+    wl = W.build_2fcnet_workload(W.WorkloadConfig(steps=5, dataset=W.DatasetConfig(search_n=320,
+                                                                                   holdout_n=64)))
+    w0 = [wl.weights[n] for n in W.WEIGHT_NAMES]
+    xb, yb = wl.search_x[0], wl.search_y[0]
+    inds = load("bench_train_pool.json.gz")["individuals"]
+    checked = used = 0
+    for ind in inds[:160]:
+        if ind.get("invalid_patch"):
+            continue
+        ts = dialect.parse_function(ind["train_step"])
+        low = Lw.lower_function(ts)
+        nw = len(ts.returns)
+        if [tuple(s) for s in low.ret_strides] != [L.c_strides(tuple(t.shape)) for t in ts.return_types]:
+            continue                     # layout-changing variants: not this test's subject
+        mask = inplace_weights(Lw.encode_instrs(low.instrs), nw)
+        outs = []
+        for alias in (False, True):
+            consts = Lw.consts_to_words(low.consts).view(np.int64).copy() if low.consts \
+                else np.zeros(1, dtype=np.int64)
+            mem = {Lw.BUF_ARENA: np.zeros(max(low.arena_elems, 1), dtype=np.int64),
+                   Lw.BUF_CONST: consts,
+                   Lw.BUF_SMEM: np.zeros(max(low.smem_elems, 1), dtype=np.int64)}
+            for k, p in enumerate(w0 + [xb, yb]):
+                mem[Lw.BUF_PARAM0 + k] = _words(p)
+            for r, ty in enumerate(ts.return_types):
+                if alias and (mask >> r) & 1:
+                    mem[Lw.BUF_OUT0 + r] = mem[Lw.BUF_PARAM0 + r]
+                else:
+                    mem[Lw.BUF_OUT0 + r] = np.zeros(max(1, int(np.prod(ty.shape))), dtype=np.int64)
+            plan_emu.run(low.instrs, mem)
+            outs.append([mem[Lw.BUF_OUT0 + r].copy() for r in range(nw)])
+        for a, b in zip(*outs):
+            assert np.array_equal(a, b), ind["key"][:60]
+        checked += 1
+        used += bin(mask).count("1")
+    assert checked >= 100 and used >= 3 * checked
