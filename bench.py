@@ -283,15 +283,16 @@ def measured_traffic(sha):
     return t.get("dram_bytes_per_launch"), t
 
 
-def cnn_measure(local, steps=1):
+def cnn_measure(local, steps=1, n_img=1000):
     """configs[2] on a bounded sample: the 16 reference-made mutants of the
     full network (tests/golden/cnn_full_pop.json.gz) x 8 = population 128,
-    scored over 1 000 synthetic CIFAR-shaped images (batch 100)."""
+    scored over `n_img` (default 1 000 of the 10 000) synthetic CIFAR-shaped
+    images (batch 100)."""
     from golden_io import load
     from paper_2310_10211_b200 import cnn, dialect
     from paper_2310_10211_b200.evaluator import DeviceEvaluator
     g = load("cnn_full_pop.json.gz")
-    n_img, batch = 1000, 100
+    batch = 100
     cfg = cnn.CnnConfig(**cnn.MOBILENETV2_CIFAR_HALF, batch_size=batch, search_n=n_img,
                         holdout_n=batch)
     wl = cnn.build_cnn_prediction_workload(cfg)
@@ -315,7 +316,7 @@ def cnn_measure(local, steps=1):
     ev.close()
     d, w = statistics.median(dev), statistics.median(wall)
     return {"workload": "configs[2]: MobileNetV2-CIFAR width 0.5, population 128 "
-                        "(16 reference-made mutants x 8), bounded sample of 1000 images "
+                        f"(16 reference-made mutants x 8), {n_img} images "
                         "(batch 100) of the 10k-image split",
             "value": 128 / d, "unit": UNIT, "images_per_s": 128 * n_img / d,
             "e2e": 128 / w, "fp64_dot_tflops": 2.0 * macs * (n_img // batch) * 128 / d / 1e12,

@@ -553,8 +553,10 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   // Training: the weight blocks move to one region, all block 0s first.
   // Block 0 is where in-place weights live for the whole launch (w1: 200 KB
   // per individual, read twice and written once per step), so one L2
-  // persisting access window covers exactly the hot weights (GEVO_B200_L2WINDOW=0
-  // turns the window off).  The window stays on the context's stream; the
+  // persisting access window can cover exactly the hot weights
+  // (GEVO_B200_L2WINDOW=1; off by default: +1 % on the bench's one launch of
+  // 256, but -30 % on the recorded 512 x 50 run's many smaller launches
+  // alternating between two contexts, profiles/r02_experiments.md).  The window stays on the context's stream; the
   // blocks are zeroed at every launch start, so lines left persisting hold no
   // input of the next launch.
   if (a.mode == GEVO_MODE_TRAIN && a.steps > 0) {
@@ -563,8 +565,10 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
     if (ctx->wreg.ensure(bytes, ctx->stream)) return fail(ctx, GEVO_E_CUDA, "weight region alloc failed");
     a.wreg = static_cast<double*>(ctx->wreg.p);
     a.n_prog = h->n_prog;
+    if (getenv("GEVO_POISON"))          // the weight region too (see the arena's poison)
+      CK(cudaMemsetAsync(ctx->wreg.p, 0xFF, bytes, ctx->stream));
     const char* ew = getenv("GEVO_B200_L2WINDOW");
-    if (!ew || atoi(ew) != 0) {
+    if (ew && atoi(ew) != 0) {
       int max_persist = 0, max_window = 0;
       cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device);
       cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device);

@@ -1066,8 +1066,13 @@ GEVO_KNAME(eval_kernel)(const __grid_constant__ EvalArgs args) {
     // A step stores each returned weight in its numpy layout; a broadcast
     // (stride-0) or otherwise compact return covers only part of its slot.
     // Zero both ping-pong blocks first so the uncovered words -- not part of
-    // any weight -- are finite for the whole-block checks below.
-    for (int i = threadIdx.x; i < 2 * wsz; i += blockDim.x) wbuf[0][i] = 0.0;
+    // any weight -- are finite for the whole-block checks below.  The two
+    // blocks are not adjacent in the launch's weight region (all block 0s,
+    // then all block 1s): zero each on its own, never a neighbour's.
+    for (int i = threadIdx.x; i < wsz; i += blockDim.x) {
+      wbuf[0][i] = 0.0;
+      wbuf[1][i] = 0.0;
+    }
     __syncthreads();
     const gevo_instr* t0 = stage(cache, args.instrs + P.train0, P.train0_n);
     const gevo_instr* cur = t0;
