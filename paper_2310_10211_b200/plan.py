@@ -151,24 +151,31 @@ def inplace_weights(arr, nw) -> int:
     W stores either way (the returned layout is a fixed point of the
     program of steps >= 1).  `arr` is the encoded table, EXT records
     included."""
-    groups, k = [], 0
-    n = len(arr)
-    while k < n:
-        r = arr[k]
-        op = int(r["op"])
-        n_ext = int(r["aux2"][0]) if op == 5 else (int(r["aux2"][4]) if op in (1, 2, 3, 8) else 0)
-        groups.append((k, n_ext))
-        k += 1 + n_ext
+    # per record: its group (the main record it belongs to; EXT records,
+    # op 7, follow their main record) and which of its operands it reads
+    ops = np.asarray(arr["op"])
+    main = ops != 7
+    grp = np.cumsum(main) - 1
+    inbuf = np.asarray(arr["in"]["buf"])                     # (n, 3)
+    nin = np.array([_NIN.get(int(o), 0) for o in ops]) if len(ops) else np.zeros(0, int)
+    live = np.where(main[:, None], np.arange(3)[None, :] < nin[:, None], True)
+    outbuf = np.asarray(arr["out"]["buf"])
+    main_idx = np.flatnonzero(main)
     mask = 0
     for w in range(nw):
         P, O = 2 + w, 2 + MAXP + w
-        writers = [g for g, (k, _) in enumerate(groups) if int(arr[k]["out"]["buf"]) == O]
+        writers = main_idx[outbuf[main_idx] == O]
         if len(writers) != 1:
             continue
-        g_w = writers[0]
-        W = arr[groups[g_w][0]]
+        k_w = int(writers[0])
+        g_w = int(grp[k_w])
+        W = arr[k_w]
         op = int(W["op"])
         if op not in (1, 2, 3, 5):
+            continue
+        reads_p = (inbuf == P) & live                            # (n, 3)
+        rec_reads = reads_p.any(axis=1)
+        if (rec_reads & (grp > g_w)).any():                      # read after the update
             continue
         rank = 2 if op == 5 else int(W["rank"])
 
@@ -184,19 +191,15 @@ def inplace_weights(arr, nw) -> int:
             return int(v["off"]), (0, st[0] if rank == 1 else 0)
         out_key = key(W["out"], False)
         ok = True
-        for g in range(g_w, len(groups)):
-            k, e = groups[g]
-            rec = arr[k]
-            reads = [rec["in"][j] for j in range(_NIN.get(int(rec["op"]), 0))]
-            ext = [arr[k + 1 + x]["in"][j] for x in range(e) for j in range(3)]
-            if g > g_w:
-                ok = not any(int(v["buf"]) == P for v in reads + ext)
-            elif op == 5 and any(int(v["buf"]) == P for v in reads):
+        for k in np.flatnonzero(rec_reads & (grp == g_w)):      # W's own reads of P
+            is_ext = not main[k]
+            if op == 5 and not is_ext:                           # a DOT operand (i, k) / (k, j)
                 ok = False
-            else:
-                ok = all(key(v, x) == out_key
-                         for v, x in ([] if op == 5 else [(v, False) for v in reads]) +
-                         [(v, True) for v in ext] if int(v["buf"]) == P)
+                break
+            for j in np.flatnonzero(reads_p[k]):
+                if key(arr[k]["in"][j], is_ext) != out_key:
+                    ok = False
+                    break
             if not ok:
                 break
         if ok:
