@@ -412,10 +412,12 @@ def build_population_plan(variants: list[VariantPlan], weight_shapes,
     hdr["max_arena"] = max_arena
     hdr["max_smem"] = max_smem
     hdr["total_elems"] = elem
-    instrs = np.concatenate(instr_chunks) if instr_chunks else \
-        np.zeros(0, dtype=INSTR_DTYPE)
+    # raw bytes: concatenating structured arrays promotes dtypes field by
+    # field (numpy _promote_fields), which cost ~30 ms per 256 individuals
+    instrs = np.concatenate([c.view(np.uint8) for c in instr_chunks]) if instr_chunks else \
+        np.zeros(0, dtype=np.uint8)
     consts = np.concatenate(const_chunks) if const_chunks else np.zeros(0)
-    blob = np.concatenate([hdr.view(np.uint8), instrs.view(np.uint8),
+    blob = np.concatenate([hdr.view(np.uint8), instrs,
                            progs.view(np.uint8), consts.view(np.uint8)])
     return PopulationPlan(blob, len(order), np.asarray(order), elem)
 
@@ -471,9 +473,9 @@ def exec_once_plan(fns, param_arrays_list):
     hdr["n_instr"], hdr["n_prog"], hdr["n_const"] = n_instr, n, n_const
     hdr["max_smem"] = max_smem
     hdr["total_elems"] = elem
-    instrs = np.concatenate(chunks) if chunks else np.zeros(0, dtype=INSTR_DTYPE)
+    instrs = np.concatenate([c.view(np.uint8) for c in chunks]) if chunks else np.zeros(0, dtype=np.uint8)
     consts = np.concatenate(consts_c) if consts_c else np.zeros(0)
-    blob = np.concatenate([hdr.view(np.uint8), instrs.view(np.uint8),
+    blob = np.concatenate([hdr.view(np.uint8), instrs,
                            progs.view(np.uint8), consts.view(np.uint8)])
     params_blob = np.concatenate(params_flat) if params_flat else np.zeros(1)
     return blob, params_blob, out_meta, max(oofs, 1)
