@@ -58,7 +58,7 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-cnn", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--no-tf32", action="store_true", help="skip the tf32 (tcgen05) side line")
+    p.add_argument("--no-tf32", action="store_true", help="skip the tf32/bf16 (tcgen05) side lines")
     return p.parse_args()
 
 
@@ -409,14 +409,19 @@ def main():
         strong = {"population": POP, "value": POP * len(s_ms) / t.item(), "unit": UNIT,
                   "ms_per_step": 1e3 * t.item() / len(s_ms), "scaling": "strong",
                   "note": "configs[1]: population 256 sharded over the GPUs (256/N per GPU)"}
-    # (1b) the reduced-precision mode on the same plans: every f64 DOT on
-    # tcgen05 (GEVO_B200_DTYPE=tf32); device time and the error's exact-match
+    # (1b) the reduced-precision modes on the same plans: every f64 DOT on
+    # tcgen05 (GEVO_B200_DTYPE=tf32, bf16); device time and the error's exact-match
     # rate against the reference -- a side line, never the headline (the
     # reference computes in float64)
-    tf32 = None
-    if not args.no_tf32:
+    tc_lines = {}
+    for mode, kind, tol in (("tf32", "kind::tf32", "per dot |err| <= 2e-3 * sum|a||b|; one train_step "
+                             "within 2e-3 normwise (tests/test_tc.py)"),
+                            ("bf16", "kind::f16", "per dot |err| <= 1e-2 * sum|a||b|; one train_step "
+                             "within 2e-2 normwise (tests/test_tc.py)")):
+        if args.no_tf32:
+            break
         t_ms, t_exact, t_n = [], 0, 0
-        os.environ["GEVO_B200_DTYPE"] = "tf32"
+        os.environ["GEVO_B200_DTYPE"] = mode
         try:
             for s in range(args.warmup, total_steps):
                 fns, vps = shard_steps[s]
@@ -435,12 +440,10 @@ def main():
                     t_exact += err == ind["error"]
         finally:
             del os.environ["GEVO_B200_DTYPE"]
-        tf32 = {"value": len(pops[0][rank::world]) * len(t_ms) / (sum(t_ms) / 1e3), "unit": UNIT,
-                "ms_per_step": statistics.mean(t_ms), "dtype": "tf32 (tcgen05.mma kind::tf32, fp32 "
-                "accumulation; every other op float64)",
-                "error_exact_vs_reference": {"exact": t_exact, "of": t_n},
-                "tolerance": "per dot |err| <= 2e-3 * sum|a||b|; one train_step within 2e-3 normwise "
-                             "(tests/test_tc.py)"}
+        tc_lines[mode] = {"value": len(pops[0][rank::world]) * len(t_ms) / (sum(t_ms) / 1e3), "unit": UNIT,
+                          "ms_per_step": statistics.mean(t_ms), "dtype": f"{mode} (tcgen05.mma {kind}, fp32 "
+                          "accumulation; every other op float64)",
+                          "error_exact_vs_reference": {"exact": t_exact, "of": t_n}, "tolerance": tol}
     # (2) e2e through the reference's seam: _Evaluator(workload)(patches)
     wall_s, h2d, d2h, e2e_launches = [], [], [], 0
     parity_ok = parity_n = 0
@@ -541,8 +544,7 @@ def main():
         }
         if cnn_line is not None:
             line["cnn"] = cnn_line
-        if tf32 is not None:
-            line["tf32"] = tf32
+        line.update(tc_lines)
         if strong is not None:
             line["strong_pop256"] = strong
         print(json.dumps(line), flush=True)

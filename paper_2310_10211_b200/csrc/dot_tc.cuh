@@ -32,21 +32,38 @@ namespace gevo {
 
 constexpr int kTcCols = 64;           // TMEM columns per CTA (fp32 accumulator): N per tile
 constexpr int kTcKC = 32;             // K per staged chunk
-constexpr uint32_t kTcSBO = (kTcKC / 4) * 128;   // bytes between 8-row groups
+constexpr uint32_t kTcSBO = (kTcKC / 4) * 128;   // bytes between 8-row groups (tf32)
 constexpr uint32_t kTcLBO = 128;                 // bytes between K core matrices
-constexpr uint32_t kTcTileA = 16 * kTcSBO;       // a 128-row A tile (16 KB)
+constexpr uint32_t kTcTileA = 16 * kTcSBO;       // a 128-row A tile (16 KB; bf16 uses half)
 constexpr uint32_t kTcTileB = (kTcCols / 8) * kTcSBO;   // a 64-column B tile (8 KB)
 
-__device__ __forceinline__ uint64_t tc_desc(uint32_t addr) {
+// per element type: bytes per element, elements per 16-byte core-matrix row,
+// SBO (bytes between 8-row groups of a KC-wide chunk), K of one MMA
+template <bool BF> struct TcFmt {
+  static constexpr int ES = BF ? 2 : 4;
+  static constexpr int EPC = 16 / ES;
+  static constexpr uint32_t SBO = (kTcKC / EPC) * 128;
+  static constexpr int MMA_K = BF ? 16 : 8;
+};
+
+__device__ __forceinline__ uint64_t tc_desc(uint32_t addr, uint32_t sbo = kTcSBO) {
   uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
   d |= (uint64_t)((kTcLBO >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((kTcSBO >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;             // descriptor version (sm_100); SWIZZLE_NONE
   return d;
 }
 
-__device__ __forceinline__ uint32_t tc_idesc(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// D f32; A, B tf32 (format 2, kind::tf32) or bf16 (format 1, kind::f16); K-major
+__device__ __forceinline__ uint32_t tc_idesc(int M, int N, bool bf = false) {
+  const uint32_t f = bf ? 1u : 2u;
+  return (1u << 4) | (f << 7) | (f << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ uint32_t bf16_bits(double x) {
+  unsigned short h;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"((float)x));
+  return h;
 }
 
 __device__ __forceinline__ uint32_t tf32_bits(double x) {
@@ -127,8 +144,10 @@ __device__ __forceinline__ void tc_tick(unsigned long long* prof, int ph, long l
   }
 }
 
+template <bool BF>
 __device__ __noinline__ void dot_tc(TcState& T, const DotArgs& dref, int col0, int col1, const EpiDev* epi,
                                     double* stage_buf, unsigned long long* prof) {
+  using F = TcFmt<BF>;
   const DotArgs d = dref;            // registers, not the caller's stack frame
   long long tt = clock64();
   const int M = d.M, K = d.K, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -147,7 +166,7 @@ __device__ __noinline__ void dot_tc(TcState& T, const DotArgs& dref, int col0, i
     for (int n0 = col0; n0 < col1; n0 += kTcCols) {
       const int nt = min(kTcCols, col1 - n0);
       const int ntp = (nt + 15) & ~15;
-      const uint32_t idesc = tc_idesc(128, ntp);
+      const uint32_t idesc = tc_idesc(128, ntp, BF);
       // staging slots: A 16 per thread of the 128 x 32 chunk, B 8 of the
       // 64 x 32 chunk, consecutive threads along each operand's unit-stride
       // axis; each batch of 8 slots has all its loads in flight before any
@@ -166,7 +185,7 @@ __device__ __noinline__ void dot_tc(TcState& T, const DotArgs& dref, int col0, i
       // A from the shared batch x: TMA boxes of its fp32 mirror, one per
       // core matrix (8 rows x 4 columns), issued by one thread per chunk
       int trow0 = -1;
-      if (T.tmap && mt == 32 && d.sak == 1 && d.sam == T.tcols && d.A >= T.tx64) {
+      if (!BF && T.tmap && mt == 32 && d.sak == 1 && d.sam == T.tcols && d.A >= T.tx64) {
         const int64_t off = (d.A + (int64_t)m0 * d.sam) - T.tx64;
         if (off < T.trows * (int64_t)T.tcols && off % T.tcols == 0 && (off / T.tcols) % 8 == 0 &&
             off / T.tcols + 32 <= T.trows)
@@ -213,14 +232,18 @@ __device__ __noinline__ void dot_tc(TcState& T, const DotArgs& dref, int col0, i
             const int u = u0 + j;
             if (u < 16) {
               const int m = am0 + u * amd, k = ak0 + u * akd;
-              if (m < mt)
-                *reinterpret_cast<uint32_t*>(As + (m >> 3) * kTcSBO + (k >> 2) * kTcLBO + (m & 7) * 16 + (k & 3) * 4) =
-                    tf32_bits(v[j]);
+              if (m < mt) {
+                const uint32_t o = (m >> 3) * F::SBO + (k / F::EPC) * kTcLBO + (m & 7) * 16 + (k % F::EPC) * F::ES;
+                if (BF) *reinterpret_cast<unsigned short*>(As + o) = (unsigned short)bf16_bits(v[j]);
+                else *reinterpret_cast<uint32_t*>(As + o) = tf32_bits(v[j]);
+              }
             } else {
               const int n = bn0 + (u - 16) * bnd, k = bk0 + (u - 16) * bkd;
-              if (n < ntp)
-                *reinterpret_cast<uint32_t*>(Bs + (n >> 3) * kTcSBO + (k >> 2) * kTcLBO + (n & 7) * 16 + (k & 3) * 4) =
-                    tf32_bits(v[j]);
+              if (n < ntp) {
+                const uint32_t o = (n >> 3) * F::SBO + (k / F::EPC) * kTcLBO + (n & 7) * 16 + (k % F::EPC) * F::ES;
+                if (BF) *reinterpret_cast<unsigned short*>(Bs + o) = (unsigned short)bf16_bits(v[j]);
+                else *reinterpret_cast<uint32_t*>(Bs + o) = tf32_bits(v[j]);
+              }
             }
           }
         }
@@ -235,12 +258,19 @@ __device__ __noinline__ void dot_tc(TcState& T, const DotArgs& dref, int col0, i
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a0 = sbase + 2 * kTcTileB + b * kTcTileA, b0 = sbase + b * kTcTileB;
 #pragma unroll
-          for (int kk = 0; kk < kTcKC / 8; ++kk) {
+          for (int kk = 0; kk < kTcKC / F::MMA_K; ++kk) {
             const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
-            asm volatile(
-                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(T.tmem),
-                "l"(tc_desc(a0 + kk * 2 * kTcLBO)), "l"(tc_desc(b0 + kk * 2 * kTcLBO)), "r"(idesc), "r"(acc));
+            const uint64_t da = tc_desc(a0 + kk * 2 * kTcLBO, F::SBO), db = tc_desc(b0 + kk * 2 * kTcLBO, F::SBO);
+            if (BF)
+              asm volatile(
+                  "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(T.tmem),
+                  "l"(da), "l"(db), "r"(idesc), "r"(acc));
+            else
+              asm volatile(
+                  "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                  "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(T.tmem),
+                  "l"(da), "l"(db), "r"(idesc), "r"(acc));
           }
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                        ::"r"(smem_u32(&T.mbar[b])) : "memory");

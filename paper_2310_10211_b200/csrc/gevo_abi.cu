@@ -53,19 +53,21 @@ struct DevBuf {
   }
 };
 
-// the tf32 executor build (gevo_exec_tc.cu, its own module)
+// the tcgen05 executor build (gevo_exec_tc.cu, its own module: tf32 and bf16)
 extern "C" void gevo_internal_launch_eval_tc(const void* a, int n_prog, cudaStream_t st);
 extern "C" void gevo_internal_launch_once_tc(const void* a, int n_prog, cudaStream_t st);
 
 // The DOT arithmetic (GEVO_B200_DTYPE): "f64" (default) -- float64 in the
 // reference's summation orders on DMMA, bit-exact; "tf32" -- tcgen05 tensor
-// cores with tf32 operands and fp32 accumulation (dot_tc.cuh), a
-// reduced-precision mode whose fitness is reported against the reference,
-// not gated.  -1: unknown value.
+// cores with tf32 operands and fp32 accumulation (dot_tc.cuh); "bf16" -- the
+// same with bf16 operands (kind::f16).  The last two are reduced-precision
+// modes whose fitness is reported against the reference, not gated.
+// -1: unknown value.
 int tc_mode() {
   const char* v = getenv("GEVO_B200_DTYPE");
   if (!v || !*v || !strcmp(v, "f64")) return 0;
   if (!strcmp(v, "tf32")) return 1;
+  if (!strcmp(v, "bf16")) return 2;
   return -1;
 }
 
@@ -505,7 +507,7 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   a.final_weights = final_weights ? static_cast<double*>(ctx->finalw.p) : nullptr;
   a.smem_elems = h->max_smem;
   a.tc = tc_mode();
-  if (a.tc < 0) return fail(ctx, GEVO_E_ARG, "GEVO_B200_DTYPE must be f64 or tf32");
+  if (a.tc < 0) return fail(ctx, GEVO_E_ARG, "GEVO_B200_DTYPE must be f64, tf32 or bf16");
   a.prof = nullptr;
   if (ctx->profile) {
     if (ctx->prof.ensure(GEVO_PROFILE_SLOTS * 2 * 8, ctx->stream)) return fail(ctx, GEVO_E_CUDA, "profile alloc");
@@ -518,7 +520,7 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   // tensor map over it (8 x 4 boxes = one canonical core matrix each), so the
   // tcgen05 dots take their shared A operand by cp.async.bulk.tensor
   // (dot_tc.cuh).  GEVO_B200_TMA=0 stages it with the threads instead.
-  if (a.tc && a.mode == GEVO_MODE_TRAIN && tr && tr->x && tr->features % 4 == 0) {
+  if (a.tc == 1 && a.mode == GEVO_MODE_TRAIN && tr && tr->x && tr->features % 4 == 0) {
     const char* et = getenv("GEVO_B200_TMA");
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
@@ -674,7 +676,7 @@ int gevo_exec_once(gevo_ctx* ctx, const void* plan, size_t plan_bytes, const dou
   a.params = static_cast<const double*>(ctx->params.p);
   a.outs = static_cast<double*>(ctx->outs.p);
   a.tc = tc_mode();
-  if (a.tc < 0) return fail(ctx, GEVO_E_ARG, "GEVO_B200_DTYPE must be f64 or tf32");
+  if (a.tc < 0) return fail(ctx, GEVO_E_ARG, "GEVO_B200_DTYPE must be f64, tf32 or bf16");
   a.smem_elems = h->max_smem;
   if (a.tc) gevo_internal_launch_once_tc(&a, h->n_prog, ctx->stream);
   else launch_once(a, h->n_prog, ctx->stream);

@@ -793,7 +793,8 @@ __device__ __noinline__ void run_dot(Shared& S, const gevo_instr& I, double* sta
   const bool integer = I.kin != GEVO_K_F64;
 #if GEVO_TC_MODE
   if (!integer) {                     // reduced-precision mode: every f64 dot on tcgen05
-    dot_tc(S.tc, d, 0, N, epi, stage, S.prof);
+    if (S.tc_on == 2) dot_tc<true>(S.tc, d, 0, N, epi, stage, S.prof);   // bf16
+    else dot_tc<false>(S.tc, d, 0, N, epi, stage, S.prof);            // tf32
     return;
   }
 #endif
@@ -1023,7 +1024,7 @@ GEVO_KNAME(eval_kernel)(const __grid_constant__ EvalArgs args) {
   double* smem_arena = dyn_smem + kStageElems;
   const gevo_prog P = args.progs[blockIdx.x];
   if (threadIdx.x == 0) {
-    S.tc_on = GEVO_TC_MODE;
+    S.tc_on = GEVO_TC_MODE ? args.tc : 0;
     S.prof = args.prof;
     S.tc.tmap = args.tma_x64 ? static_cast<const void*>(args.tma_map) : nullptr;
     S.tc.tx64 = args.tma_x64;
@@ -1211,7 +1212,7 @@ GEVO_KNAME(exec_once_kernel)(OnceArgs args) {
   double* smem_arena = dyn_smem + kStageElems;
   const gevo_prog P = args.progs[blockIdx.x];
   if (threadIdx.x == 0) {
-    S.tc_on = GEVO_TC_MODE;
+    S.tc_on = GEVO_TC_MODE ? args.tc : 0;
     S.prof = nullptr;
     S.base[GEVO_BUF_ARENA] = args.arena + P.arena_off;
     S.base[GEVO_BUF_SMEM] = smem_arena;
