@@ -76,11 +76,13 @@ def _lower_many(batch):
     """Worker: lower a list of variants; None for a variant that fails
     (evaluate() maps any exception to INVALID_FITNESS), the exception itself
     for a valid variant the device cannot run (raised by the caller)."""
-    fns_list, cost_table, training, steps = batch
+    fns_list, cost_table, training, steps = batch[:4]
+    fwd_memo = batch[4] if len(batch) > 4 else None
     out = []
     for fns in fns_list:
         try:
-            out.append(lower_variant(fns, cost_table, training=training, steps=steps))
+            out.append(lower_variant(fns, cost_table, training=training, steps=steps,
+                                     fwd_memo=fwd_memo))
         except UnsupportedVariant as e:
             out.append(e)
         except Exception:
@@ -96,16 +98,25 @@ def _lower_patches(batch):
     token, keys, functions, cost_table, training, steps = batch
     from evotir.genome import PatchApplicationError, apply_patch, patch_loads
     original = _MODULES[token]
+    # a patch that edits no op of @forward leaves it the original's function:
+    # its encoded lowering is shared per (module, cost table, weight layout)
+    memo = _FWD_MEMO.setdefault((token, repr(sorted(cost_table.items())) if cost_table else None,
+                                 training, steps), {})
     out = []
     for key in keys:
         try:
-            m = apply_patch(original, patch_loads(key)).module
+            patch = patch_loads(key)
+            m = apply_patch(original, patch).module
         except PatchApplicationError:
             out.append(None)
             continue
+        untouched = "forward" in functions and all(e.function != "forward" for e in patch)
         out.extend(_lower_many(([{n: m.functions[n] for n in functions}],
-                                cost_table, training, steps)))
+                                cost_table, training, steps, memo if untouched else None)))
     return out
+
+
+_FWD_MEMO: dict = {}      # per worker process: see _lower_patches
 
 
 def _check_supported(vp):

@@ -52,11 +52,16 @@ def _count(shape):
 
 
 def lower_variant(functions: dict, cost_table=None, training=True,
-                  weight_layouts=None, steps: int = 600) -> VariantPlan:
+                  weight_layouts=None, steps: int = 600, fwd_memo: dict | None = None) -> VariantPlan:
     """functions: {'train_step': fn, 'forward': fn} (train_step only in
     training mode).  Weight params start C-ordered like the module
     constants; steps >= 1 see the layout the previous step stored, and
-    @forward is lowered for the layout after `steps` training steps."""
+    @forward is lowered for the layout after `steps` training steps.
+
+    fwd_memo: given only when `forward` is the same function for every
+    variant lowered through this dict (a patch that edits no op of @forward,
+    genome.py:482-516, with one cost table): the encoded forward is then
+    reused per weight layout instead of lowered again."""
     consts: list = []
     arena = 0
     smem = 0
@@ -124,12 +129,21 @@ def lower_variant(functions: dict, cost_table=None, training=True,
     f_layout = [L.c_strides(tuple(t.shape)) for _, t in fw.params]
     if fwd_layouts is not None:
         f_layout[:nwf] = fwd_layouts[:nwf]
-    lowf = lower_function(fw, f_layout, ret_layout="c", cost_table=cost_table)
-    f = _encode_shifted(lowf, consts)
-    arena = max(arena, lowf.arena_elems)
-    smem = max(smem, lowf.smem_elems)
+    key = tuple(tuple(x) for x in f_layout)
+    hit = fwd_memo.get(key) if fwd_memo is not None else None
+    if hit is None:
+        lowf = lower_function(fw, f_layout, ret_layout="c", cost_table=cost_table)
+        arr = encode_instrs(lowf.instrs)
+        hit = (list(lowf.consts), arr, lowf.arena_elems, lowf.smem_elems, lowf.cost, fn_weight(arr))
+        if fwd_memo is not None:
+            fwd_memo[key] = hit
+    f_consts, f_arr, f_arena, f_smem, f_cost, f_weight = hit
+    f = _shift_consts(f_arr.copy(), len(consts))
+    consts.extend(f_consts)
+    arena = max(arena, f_arena)
+    smem = max(smem, f_smem)
     return VariantPlan(t0, t1, f, consts_to_words(consts), arena, smem, flags,
-                       train_cost, lowf.cost, fn_weight(t1), fn_weight(f), t2)
+                       train_cost, f_cost, fn_weight(t1), f_weight, t2)
 
 
 # in-place weight updates (inplace_weights); GEVO_B200_INPLACE=0 turns them off
@@ -212,7 +226,11 @@ def _encode_shifted(low, pool):
     individual's pool (CONST operand offsets rebased)."""
     base = len(pool)
     pool.extend(low.consts)
-    arr = encode_instrs(low.instrs)
+    return _shift_consts(encode_instrs(low.instrs), base)
+
+
+def _shift_consts(arr, base):
+    """Rebase the CONST operand offsets of an encoded function by `base`."""
     if base:
         for slot in ("out", "in"):
             bufs = arr[slot]["buf"]

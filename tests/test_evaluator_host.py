@@ -219,3 +219,43 @@ def test_scratch_budget_splits_a_half_into_sequential_launches(fake, monkeypatch
         else:
             assert f.error == r["wrong"] / 992
     ev.close()
+
+
+def test_forward_memo_identical_plans():
+    """The patch workers share the encoded @forward of every patch that edits
+    no op of it (plan.lower_variant fwd_memo): the plans are byte-identical
+    to lowering each variant on its own, for patches that do and do not
+    touch @forward, in any order."""
+    import pytest
+    from golden_io import reference_available
+    if not reference_available():
+        pytest.skip("reference not importable")
+    import numpy as np
+    from evotir import fitness as F
+    from evotir.genome import patch_loads
+    from paper_2310_10211_b200 import evaluator as E
+    inds = [i for i in load("bench_train_pool.json.gz")["individuals"] if not i.get("invalid_patch")]
+    keys = [i["key"] for i in inds[:80]]
+    touched = [any(e.function == "forward" for e in patch_loads(k)) for k in keys]
+    assert any(touched) and not all(touched)
+    wl = F.build_2fcnet_workload()
+    tok = E.register_module(wl.module)
+    fns = ("train_step", "forward")
+    E._FWD_MEMO.clear()
+    shared = E._lower_patches((tok, keys, fns, None, True, 600))
+    assert E._FWD_MEMO and any(len(m) for m in E._FWD_MEMO.values())
+    alone = []
+    for k in keys:
+        E._FWD_MEMO.clear()
+        alone += E._lower_patches((tok, [k], fns, None, True, 600))
+    for a, b in zip(shared, alone):
+        assert (a is None) == (b is None)
+        if a is None:
+            continue
+        for f in ("train0", "train1", "fwd", "consts", "train2"):
+            x, y = getattr(a, f), getattr(b, f)
+            assert (x is None) == (y is None)
+            if x is not None:
+                assert x.tobytes() == y.tobytes(), f
+        for f in ("arena", "smem", "flags", "train_cost", "fwd_cost", "w_train", "w_fwd"):
+            assert getattr(a, f) == getattr(b, f), f
