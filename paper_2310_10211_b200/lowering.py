@@ -163,11 +163,20 @@ def dot_modes(a: Val, b: Val):
     tn = trans_b and not trans_a
     small = _small_kernel(m, k, n, tn)
     if small and tn:
-        return D_ACC8_TREE, n - n % 8, D_ACC8_TREE, corner
+        # the TN kernel's n % 8 edge runs a 4-column sub-kernel first (its
+        # m % 4 rows reduce by the pairwise tree) when n % 8 >= 4; the AVX-512
+        # corner is in the columns after it
+        return D_ACC8_TREE, n - n % 8 + (4 if n % 8 >= 4 else 0), D_ACC8_TREE, corner
     if small and not trans_a and not trans_b and n % 8 and k >= 16:
-        # the n % 8 edge columns of the NN small kernel: 8 lane chains once
-        # K >= 16 (the blocked kernels below keep one chain per output)
-        return D_FMA_CHAIN, n - n % 8, D_ACC8_TREE, corner
+        # the n % 8 edge columns of the NN small kernel once K >= 16 (the
+        # blocked kernels below keep one chain per output): 8 lane chains
+        # when n % 8 <= 4 -- reduced in the AVX-512 order in the m % 4 rows
+        # for n % 8 < 4, by the pairwise tree in every row for n % 8 == 4 --
+        # and one k-ordered chain per output for n % 8 >= 5 (probed on
+        # numpy / OpenBLAS here, tests/test_dot_orders.py)
+        if n % 8 >= 5:
+            return D_FMA_CHAIN, n, D_FMA_CHAIN, m
+        return D_FMA_CHAIN, n - n % 8, D_ACC8_TREE, (m if n % 8 == 4 else corner)
     return D_FMA_CHAIN, n, D_FMA_CHAIN, m
 
 

@@ -11,9 +11,9 @@ copied by numpy in KEEPORDER before BLAS (found by the whole-run replay,
 tests/test_ga_replay.py: 25 of 19 970 recorded individuals).  Shapes are the
 rows from 3 to 784, n % 8 in {0, 1, 2, 3}; in the n % 8 edge columns the
 m % 4 remainder rows reduce their lanes in the AVX-512 order (the `xrow`
-corner).  Wider edges (n % 8 >= 4) go through further OpenBLAS sub-kernels
-that the rule does not model; the workloads' dots have n in {1, 10, 32, 784}
-(n % 8 in {0, 1, 2}).
+corner).  Wider edges: n % 8 == 4 keeps the 8 lane chains but reduces them
+by the pairwise tree in every row; n % 8 in {5, 6, 7} runs one k-ordered
+chain per edge output (probed here over random NN/TN shapes).
 """
 from fractions import Fraction
 
@@ -88,7 +88,11 @@ KINDS = ("C", "T", "b0", "b1", "s")
 @pytest.mark.parametrize("shape", [(32, 10, 32), (32, 32, 10), (32, 32, 32), (784, 32, 32),
                                    (32, 784, 32), (10, 32, 32), (32, 13, 32),
                                    (32, 10, 10), (10, 32, 10), (7, 32, 9), (10, 32, 9),
-                                   (3, 32, 3), (11, 40, 11), (6, 32, 17)])
+                                   (3, 32, 3), (11, 40, 11), (6, 32, 17),
+                                   # wider edges: n % 8 == 4 (8 lane chains, tree in
+                                   # every row) and n % 8 in {5, 6, 7} (one chain)
+                                   (13, 40, 12), (9, 20, 20), (13, 37, 13), (16, 33, 14),
+                                   (12, 40, 15), (5, 17, 6), (7, 48, 13)])
 def test_dot_orders_all_view_kinds(shape):
     rng = np.random.default_rng(sum(shape))
     for ka in KINDS:
@@ -98,7 +102,8 @@ def test_dot_orders_all_view_kinds(shape):
 
 def test_dot_orders_k_thresholds():
     rng = np.random.default_rng(7)
-    for m, n in ((32, 10), (10, 10), (7, 9), (32, 3), (32, 32), (10, 32), (784, 10)):
+    for m, n in ((32, 10), (10, 10), (7, 9), (32, 3), (32, 32), (10, 32), (784, 10),
+                 (13, 12), (9, 13), (7, 14), (11, 15), (5, 20)):
         for k in list(range(2, 41)) + [48, 64, 100]:
             for ka, kb in (("C", "C"), ("C", "T"), ("T", "C"), ("T", "T")):
                 check(rng, m, k, n, ka, kb)
