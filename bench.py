@@ -29,7 +29,6 @@ process pool on every host core.
 from __future__ import annotations
 
 import argparse
-import hashlib
 import json
 import os
 import statistics
@@ -264,16 +263,18 @@ def run_reference(args, world, rank):
 # ---------------------------------------------------------------------------
 
 def lib_sha():
-    from paper_2310_10211_b200 import _lib
-    with open(_lib.LIB_PATH, "rb") as f:
-        return hashlib.sha256(f.read()).hexdigest()[:16]
+    """Identity of the running build: the hash of the sources and nvcc flags
+    libgevo.so is compiled from (build.source_sha; the .so bytes differ per
+    nvcc run)."""
+    from paper_2310_10211_b200 import build
+    return build.source_sha()
 
 
 def measured_traffic(sha):
     """ncu dram bytes of the hot kernel per launch, recorded by
     tests/tools/ncu_traffic.py for THIS build of libgevo.so (profiles/
-    traffic.json carries the sha of the library it measured); null when the
-    capture is of another build."""
+    traffic.json carries the source sha of the build it measured); null when
+    the capture is of another build."""
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
     except (OSError, ValueError):

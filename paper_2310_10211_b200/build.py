@@ -17,12 +17,28 @@ LIB = os.path.join(PKG, "libgevo.so")
 SOURCES = ["gevo_exec.cu", "gevo_exec_tc.cu", "nsga2.cu", "splits.cu", "gevo_abi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC"]
 
 
 def _deps():
     files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     files += [os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE)]
     return files
+
+
+def source_sha(defines=()) -> str:
+    """Hash of everything the library is compiled from (csrc/, include/, the
+    nvcc flags): the identity of a build.  The .so bytes themselves differ
+    from one nvcc run to the next (temporary file names end up in the
+    image), so measurements recorded for a build (profiles/traffic.json)
+    are stamped with this."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in sorted(_deps()):
+        if f.endswith((".cu", ".cuh", ".h")):
+            h.update(os.path.basename(f).encode() + b"\0" + open(f, "rb").read())
+    h.update(" ".join([*ARCH, *FLAGS, *[f"-D{d}" for d in defines]]).encode())
+    return h.hexdigest()[:16]
 
 
 def needs_build() -> bool:
@@ -40,8 +56,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out=None) -> s
         return LIB
     import tempfile
     from concurrent.futures import ThreadPoolExecutor
-    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
-             "-I", INCLUDE, "-I", CSRC, *[f"-D{d}" for d in defines]]
+    flags = [*ARCH, *FLAGS, "-I", INCLUDE, "-I", CSRC, *[f"-D{d}" for d in defines]]
     if verbose:
         flags += ["-Xptxas", "-v"]
     with tempfile.TemporaryDirectory() as tmp:

@@ -1,13 +1,12 @@
 """Record the hot kernel's DRAM traffic and pipe counters from one `ncu --set
-full` capture into profiles/traffic.json, stamped with the sha of the
-libgevo.so that was profiled.  bench.py reports `roofline.traffic` only when
-that sha matches the library it is running (a capture of another build reads
-as null, never as a stale number).
+full` capture into profiles/traffic.json, stamped with the source sha of the
+build that was profiled (build.source_sha: sources + nvcc flags).  bench.py
+reports `roofline.traffic` only when that sha matches the build it is running
+(a capture of another build reads as null, never as a stale number).
 
     python tests/tools/ncu_traffic.py gpurun_out/<tag>_prof.ncu-rep <tag> [lib_sha]
 """
 import csv
-import hashlib
 import json
 import os
 import subprocess
@@ -36,8 +35,9 @@ def num(v):
 
 def main(rep, tag, sha=None):
     if sha is None:
-        lib = os.path.join(ROOT, "paper_2310_10211_b200", "libgevo.so")
-        sha = hashlib.sha256(open(lib, "rb").read()).hexdigest()[:16]
+        sys.path.insert(0, ROOT)
+        from paper_2310_10211_b200 import build
+        sha = build.source_sha()
     launches = raw_metrics(rep)
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     out = []
