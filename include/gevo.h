@@ -47,6 +47,9 @@
  *                                   context's stream)
  *   gevo_span_ms                 -- (no analogue: device span of a
  *                                   generation split over two contexts)
+ *   gevo_range_push /            -- (no analogue: the reference has only
+ *   gevo_range_pop                  wall time, search.py:342,396) NVTX
+ *                                   ranges for nsys / ncu timelines
  *
  * Conventions: every call returns 0 on success and a negative GEVO_E_* code
  * on failure (then gevo_last_error explains); no C++ exception crosses the
@@ -213,6 +216,14 @@ int gevo_comm_unique_id(void* out, size_t len);
 int gevo_comm_init(gevo_ctx* ctx, int rank, int world, const void* uid, size_t len);
 int gevo_allgather(gevo_ctx* ctx, const void* send, size_t bytes, void* recv);
 int gevo_comm_destroy(gevo_ctx* ctx);
+
+/* NVTX ranges (header-only NVTX 3: free unless a tool such as nsys or ncu
+ * --nvtx is attached).  The library itself marks gevo_eval (plan upload,
+ * launch + wait), gevo_exec_once, the NSGA-II / archive / hypervolume calls
+ * and gevo_allgather; the host pushes one range per generation and chunk.
+ * Ranges nest per calling thread. */
+int gevo_range_push(const char* name);
+int gevo_range_pop(void);
 
 /* device and build info, e.g. "NVIDIA B200 sm_100 148 SMs" */
 int gevo_device_info(gevo_ctx* ctx, char* buf, size_t len);

@@ -83,6 +83,8 @@ SIGNATURES = {
     "gevo_allgather": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                       ctypes.c_void_p]),
     "gevo_comm_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "gevo_range_push": (ctypes.c_int, [ctypes.c_char_p]),
+    "gevo_range_pop": (ctypes.c_int, []),
 }
 
 NCCL_UID_BYTES = 128
@@ -120,6 +122,23 @@ def load():
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+class nvtx_range:
+    """`with nvtx_range("generation 3"):` -- an NVTX range around the block
+    (gevo_range_push / gevo_range_pop; free unless nsys or ncu --nvtx is
+    attached)."""
+
+    def __init__(self, name: str):
+        self.name = name.encode()
+
+    def __enter__(self):
+        load().gevo_range_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        load().gevo_range_pop()
+        return False
 
 
 def ptr(a: np.ndarray, ctype=ctypes.c_double):

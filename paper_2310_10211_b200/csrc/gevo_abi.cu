@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -21,6 +22,13 @@
 using namespace gevo;
 
 namespace {
+
+// one NVTX range for the lifetime of a scope (NVTX 3 is header-only: a
+// push/pop costs a branch unless a tool is attached)
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+};
 
 struct Split {
   double* x = nullptr;         // [nb, B, F]
@@ -403,6 +411,7 @@ int gevo_upload_weights(gevo_ctx* ctx, const double* w, int64_t n_elems) {
 
 int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
               const gevo_eval_desc* desc, gevo_result* results, double* final_weights) {
+  Range nvtx_range("gevo_eval");
   if (!ctx) return GEVO_E_ARG;
   if (!desc || !results) return fail(ctx, GEVO_E_ARG, "null desc/results");
   CK(cudaSetDevice(ctx->device));
@@ -462,7 +471,10 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   const gevo_instr* di;
   const gevo_prog* dp;
   const double* dc;
-  rc = upload_plan(ctx, plan, plan_bytes, v, &di, &dp, &dc);
+  {
+    Range r("plan upload");
+    rc = upload_plan(ctx, plan, plan_bytes, v, &di, &dp, &dc);
+  }
   if (rc) return rc;
   if (ctx->arena.ensure((size_t)h->total_elems * sizeof(double) + 64, ctx->stream))
     return fail(ctx, GEVO_E_CUDA, "arena alloc failed");
@@ -598,6 +610,7 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
       }
     }
   }
+  Range launch_range(a.tc ? "eval_kernel_tc launch + wait" : "eval_kernel launch + wait");
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
   if (a.tc) gevo_internal_launch_eval_tc(&a, h->n_prog, ctx->stream);
   else launch_eval(a, h->n_prog, ctx->stream);
@@ -615,6 +628,17 @@ int gevo_eval(gevo_ctx* ctx, const void* plan, size_t plan_bytes,
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   ctx->last_ms = ms;
+  return GEVO_OK;
+}
+
+int gevo_range_push(const char* name) {
+  if (!name) return GEVO_E_ARG;
+  nvtxRangePushA(name);
+  return GEVO_OK;
+}
+
+int gevo_range_pop(void) {
+  nvtxRangePop();
   return GEVO_OK;
 }
 
@@ -649,6 +673,7 @@ int gevo_span_ms(gevo_ctx* first, gevo_ctx* second, double* ms) {
 
 int gevo_exec_once(gevo_ctx* ctx, const void* plan, size_t plan_bytes, const double* params,
                    size_t param_words, double* outs, size_t out_words) {
+  Range nvtx_range("gevo_exec_once");
   if (!ctx) return GEVO_E_ARG;
   if (!params || !outs) return fail(ctx, GEVO_E_ARG, "null params/outs");
   CK(cudaSetDevice(ctx->device));
@@ -742,6 +767,7 @@ static int nsga2_common(gevo_ctx* ctx, const double* cost, const double* error, 
 
 int gevo_archive_merge(gevo_ctx* ctx, const double* cost, const double* error, int n,
                        int32_t* keep, int32_t* n_keep) {
+  Range nvtx_range("gevo_archive_merge");
   if (!ctx) return GEVO_E_ARG;
   if (n < 0 || (n > 0 && (!cost || !error || !keep)) || !n_keep)
     return fail(ctx, GEVO_E_ARG, "bad archive_merge arguments");
@@ -773,6 +799,7 @@ int gevo_archive_merge(gevo_ctx* ctx, const double* cost, const double* error, i
 
 int gevo_hypervolume(gevo_ctx* ctx, const double* cost, const double* error, int n,
                      double ref_cost, double ref_error, double* out) {
+  Range nvtx_range("gevo_hypervolume");
   if (!ctx) return GEVO_E_ARG;
   if (n < 0 || (n > 0 && (!cost || !error)) || !out)
     return fail(ctx, GEVO_E_ARG, "bad hypervolume arguments");
@@ -805,18 +832,21 @@ int gevo_hypervolume(gevo_ctx* ctx, const double* cost, const double* error, int
 int gevo_nsga2_rank(gevo_ctx* ctx, const double* cost, const double* error, int n,
                     int32_t* rank, double* crowding, int32_t* front_order,
                     int32_t* front_start, int32_t* n_fronts) {
+  Range nvtx_range("gevo_nsga2_rank");
   return nsga2_common(ctx, cost, error, n, 0, nullptr, rank, crowding, front_order,
                       front_start, n_fronts);
 }
 
 int gevo_nsga2_crowding(gevo_ctx* ctx, const double* cost, const double* error, int n,
                         double* crowding) {
+  Range nvtx_range("gevo_nsga2_crowding");
   return nsga2_common(ctx, cost, error, n, 0, nullptr, nullptr, crowding, nullptr, nullptr,
                       nullptr, 1);
 }
 
 int gevo_nsga2_select(gevo_ctx* ctx, const double* cost, const double* error, int n,
                       int keep, int32_t* chosen, int32_t* rank, double* crowding) {
+  Range nvtx_range("gevo_nsga2_select");
   if (keep < 0 || keep > n) return fail(ctx, GEVO_E_ARG, "keep out of range");
   return nsga2_common(ctx, cost, error, n, keep, chosen, rank, crowding, nullptr, nullptr,
                       nullptr);
@@ -913,6 +943,7 @@ int gevo_comm_destroy(gevo_ctx* ctx) {
 }
 
 int gevo_allgather(gevo_ctx* ctx, const void* send, size_t bytes, void* recv) {
+  Range nvtx_range("gevo_allgather");
   if (!ctx) return GEVO_E_ARG;
   if (!ctx->comm) return fail(ctx, GEVO_E_STATE, "gevo_comm_init has not been called");
   if ((!send || !recv) && bytes) return fail(ctx, GEVO_E_ARG, "null buffer");

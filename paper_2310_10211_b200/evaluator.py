@@ -283,7 +283,12 @@ class DeviceEvaluator:
                           return_records=False, _patches=None):
         """variants: list of {'train_step': fn, 'forward': fn} (or None for
         a patch that failed to apply).  Returns list[Fitness] (and the raw
-        device records when return_records)."""
+        device records when return_records).  One NVTX range per call."""
+        with _lib.nvtx_range(f"evaluate {len(variants)} individuals"
+                             + (" (holdout)" if holdout else "")):
+            return self._evaluate_variants(variants, holdout, want_weights, return_records, _patches)
+
+    def _evaluate_variants(self, variants, holdout, want_weights, return_records, _patches):
         wl = self.workload
         cfg = wl.config
         training = wl.mode == TRAINING
@@ -362,7 +367,8 @@ class DeviceEvaluator:
                 try:
                     recs, fws, od, ms = [], [], None, 0.0
                     for plan, order_, n_g in pl:
-                        res, fw = c.eval(plan.blob, plan.n_prog, *ma)
+                        with _lib.nvtx_range(f"chunk {key}: {n_g} individuals"):
+                            res, fw = c.eval(plan.blob, plan.n_prog, *ma)
                         ms += c.last_kernel_ms()
                         recs.append(res[:n_g])
                         fws.append(fw[:n_g] if fw is not None else None)

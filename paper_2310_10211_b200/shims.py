@@ -412,6 +412,9 @@ def install(device: int | None = None, nsga2: bool = True, backend_factory=None)
     _, _, S = _E()
     if device is None:
         device = int(os.environ.get("LOCAL_RANK", "0"))
+    # GEVO_B200_NSGA2=0 keeps the reference's host NSGA-II / archive /
+    # hypervolume (the evaluator seams are rebound either way)
+    nsga2 = nsga2 and os.environ.get("GEVO_B200_NSGA2", "1") != "0"
     _NS_DEVICE = device
     if not _SAVED:
         _SAVED.update({

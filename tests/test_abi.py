@@ -41,6 +41,16 @@ def test_null_context_is_an_error_not_a_crash():
     assert lib.gevo_last_error(None) == b"null context"
 
 
+def test_nvtx_ranges_need_no_device():
+    """gevo_range_push / gevo_range_pop (NVTX 3, header-only) are callable
+    without a GPU or a profiler attached, and nest."""
+    lib = _lib.load()
+    with _lib.nvtx_range("outer"):
+        with _lib.nvtx_range("inner"):
+            pass
+    assert lib.gevo_range_push(None) < 0
+
+
 def test_plan_struct_sizes_match_header():
     from paper_2310_10211_b200 import lowering as Lw
     hdr = open(os.path.join(ROOT, "include", "gevo_plan.h")).read()

@@ -107,6 +107,22 @@ def test_install_rebinds_and_restores():
 
 
 @pytest.mark.skipif(not HAVE_REF, reason="reference package not importable")
+def test_install_host_nsga2_switch(monkeypatch):
+    """GEVO_B200_NSGA2=0 rebinds only the evaluator seams: NSGA-II, the
+    archive and the hypervolume stay the reference's host code."""
+    import evotir.search as S
+    from paper_2310_10211_b200 import shims
+    ref = (S.nondominated_sort, S.select_survivors, S.Archive, S.hypervolume)
+    monkeypatch.setenv("GEVO_B200_NSGA2", "0")
+    shims.install()
+    try:
+        assert issubclass(S._Evaluator, shims.GpuEvaluator) and S.evaluate is shims.evaluate
+        assert (S.nondominated_sort, S.select_survivors, S.Archive, S.hypervolume) == ref
+    finally:
+        shims.uninstall()
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="reference package not importable")
 def test_evaluate_seam_invalid_patch_and_holdout_reads():
     from evotir import fitness as F
     from evotir.genome import DeleteEdit, Rebind
