@@ -1,4 +1,5 @@
 # compute-sanitizer over the kernels: memcheck, racecheck
+# NOTE: compute-sanitizer is closed on the graft GPU pool ("Tracing, checks and switches"); this script is for other machines.
 # (shared-memory hazards), synccheck (barrier misuse), initcheck (reads of
 # uninitialised device memory) on tests/tools/sanitize_run.py, float64 and
 # tf32 modes.  usage: bash tests/tools/sanitize.sh [tag]
