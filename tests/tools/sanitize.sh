@@ -1,8 +1,8 @@
 # compute-sanitizer over the kernels: memcheck, racecheck
-# NOTE: compute-sanitizer is closed on the graft GPU pool (DESIGN.md §6, "Tracing, checks and switches"); this script is for other machines.
 # (shared-memory hazards), synccheck (barrier misuse), initcheck (reads of
 # uninitialised device memory) on tests/tools/sanitize_run.py, float64 and
 # tf32 modes.  usage: bash tests/tools/sanitize.sh [tag]
+# NOTE: compute-sanitizer is closed on the graft GPU pool (DESIGN.md §6, "Tracing, checks and switches"); this script is for other machines.
 TAG=${1:-san}
 for tool in memcheck racecheck synccheck initcheck; do
   for dt in f64 tf32; do
