@@ -24,6 +24,17 @@ records the BASELINE.json configs[2] network itself (MobileNetV2-CIFAR width
 0.5, cnn.MOBILENETV2_CIFAR_HALF, batch 100) over 100 images with 16
 reference-made mutants (about 10 min on one core) into
 tests/golden/cnn_full_pop.json.gz.
+
+    ... make_cnn_golden.py full2 SEED N OUT
+
+records N more full-size mutants from rng seed SEED (chains of up to five
+edits) into OUT; tests/golden/cnn_full_pop2.json.gz merges four such runs
+(seeds 2311-2314, 9 variants each, the unmutated network dropped from all
+but the first), run in parallel:
+
+    for s in 2311 2312 2313 2314; do python tests/golden/make_cnn_golden.py \
+        full2 $s 10 /tmp/cnn2_$s.json.gz & done; wait
+    python tests/golden/make_cnn_golden.py merge2 /tmp/cnn2_23*.json.gz
 """
 from __future__ import annotations
 
@@ -56,7 +67,7 @@ def fn_text(fn) -> str:
     return print_module(Module(functions={fn.name: fn}, constants={}))
 
 
-def main(full=False):
+def main(full=False, seed=2310, n_variants=N_VARIANTS, max_edits=MAX_EDITS, path=None):
     if full:
         cfg = cnn.CnnConfig(**cnn.MOBILENETV2_CIFAR_HALF, batch_size=100, search_n=100,
                             holdout_n=100)
@@ -94,13 +105,13 @@ def main(full=False):
         return dict(wrong=wrong, total=total, status=0, error=wrong / total,
                     cost=plan.total_cost * len(xs))
 
-    rng = random.Random(2310)
+    rng = random.Random(seed)
     inds = []
     patch = ()
     variants = [()]
-    while len(variants) < N_VARIANTS:
+    while len(variants) < n_variants:
         base = variants[rng.randrange(len(variants))] if len(variants) > 1 else ()
-        if len(base) >= MAX_EDITS:
+        if len(base) >= max_edits:
             base = ()
         variant = apply_patch(module, base).module
         try:
@@ -127,11 +138,35 @@ def main(full=False):
            "individuals": inds}
     if full:
         out["config"]["network"] = "MOBILENETV2_CIFAR_HALF"
-    path = os.path.join(HERE, "cnn_full_pop.json.gz" if full else "cnn_pop.json.gz")
+    path = path or os.path.join(HERE, "cnn_full_pop.json.gz" if full else "cnn_pop.json.gz")
     with gzip.open(path, "wt") as f:
         json.dump(out, f, separators=(",", ":"), sort_keys=True)
     print(f"wrote {path} ({os.path.getsize(path)} bytes)")
 
 
+def merge2(paths):
+    """cnn_full_pop2.json.gz: the full2 runs' mutants (one unmutated network)."""
+    out, seen = None, set()
+    for p in sorted(paths):
+        with gzip.open(p, "rt") as f:
+            d = json.load(f)
+        if out is None:
+            out = {"config": d["config"], "individuals": []}
+        for ind in d["individuals"]:
+            if ind["key"] not in seen:
+                seen.add(ind["key"])
+                out["individuals"].append(ind)
+    path = os.path.join(HERE, "cnn_full_pop2.json.gz")
+    with gzip.open(path, "wt") as f:
+        json.dump(out, f, separators=(",", ":"), sort_keys=True)
+    print(f"wrote {path}: {len(out['individuals'])} individuals")
+
+
 if __name__ == "__main__":
-    main(full=sys.argv[1:2] == ["full"])
+    if sys.argv[1:2] == ["full2"]:
+        main(full=True, seed=int(sys.argv[2]), n_variants=int(sys.argv[3]), max_edits=5,
+             path=sys.argv[4])
+    elif sys.argv[1:2] == ["merge2"]:
+        merge2(sys.argv[2:])
+    else:
+        main(full=sys.argv[1:2] == ["full"])

@@ -74,9 +74,12 @@ def test_device_matches_reference_on_mutants(wl, golden):
 # 16 reference-made mutants over 100 images (tests/golden/cnn_full_pop.json.gz,
 # make_cnn_golden.py full), with the reference's batch-0 probabilities
 
-@pytest.fixture(scope="module")
-def full_golden():
-    return load("cnn_full_pop.json.gz")
+@pytest.fixture(scope="module", params=["cnn_full_pop.json.gz", "cnn_full_pop2.json.gz"])
+def full_golden(request):
+    """The 16 mutants of the first recording, then the further reference-made
+    mutants (chains of up to five edits, four seeds) of make_cnn_golden.py
+    full2 / merge2."""
+    return load(request.param)
 
 
 @pytest.fixture(scope="module")
@@ -99,6 +102,8 @@ def test_full_network_mutants_cost_and_oracle(full_wl, full_golden):
     from oracle import interp as OI
     inds = full_golden["individuals"]
     assert len(inds) >= 16 and sum(i["edits"] > 0 for i in inds) >= 15
+    keys = [i["key"] for i in inds]
+    assert len(set(keys)) == len(keys)
     xb = full_wl.search_x.reshape(-1, 100, 32, 32, 3)[0]
     for k, ind in enumerate(inds):
         fn = dialect.parse_function(ind["forward"])
