@@ -284,21 +284,27 @@ def measured_traffic(sha):
     return t.get("dram_bytes_per_launch"), t
 
 
-def cnn_measure(local, steps=1, n_img=1000):
+def cnn_measure(local, steps=1, n_img=1000, pop=128, fixtures=("cnn_full_pop.json.gz",)):
     """configs[2] on a bounded sample: the 16 reference-made mutants of the
     full network (tests/golden/cnn_full_pop.json.gz) x 8 = population 128,
     scored over `n_img` (default 1 000 of the 10 000) synthetic CIFAR-shaped
-    images (batch 100)."""
+    images (batch 100).  `pop` / `fixtures`: other populations cycled over the
+    mutants of the given recordings (tests/tools/cnn_sweep.py)."""
     from golden_io import load
     from paper_2310_10211_b200 import cnn, dialect
     from paper_2310_10211_b200.evaluator import DeviceEvaluator
-    g = load("cnn_full_pop.json.gz")
+    inds, seen = [], set()
+    for fx in fixtures:
+        for i in load(fx)["individuals"]:
+            if i["key"] not in seen:
+                seen.add(i["key"])
+                inds.append(i)
     batch = 100
     cfg = cnn.CnnConfig(**cnn.MOBILENETV2_CIFAR_HALF, batch_size=batch, search_n=n_img,
                         holdout_n=batch)
     wl = cnn.build_cnn_prediction_workload(cfg)
-    base = [{"forward": dialect.parse_function(i["forward"])} for i in g["individuals"]]
-    variants = [base[k % len(base)] for k in range(128)]
+    base = [{"forward": dialect.parse_function(i["forward"])} for i in inds]
+    variants = [base[k % len(base)] for k in range(pop)]
     fn = base[0]["forward"]
     macs, types = 0, dict(fn.params)
     for op in fn.ops:
@@ -316,11 +322,11 @@ def cnn_measure(local, steps=1, n_img=1000):
         dev.append(ev.last_device_ms / 1e3)
     ev.close()
     d, w = statistics.median(dev), statistics.median(wall)
-    return {"workload": "configs[2]: MobileNetV2-CIFAR width 0.5, population 128 "
-                        f"(16 reference-made mutants x 8), {n_img} images "
+    return {"workload": f"configs[2]: MobileNetV2-CIFAR width 0.5, population {pop} "
+                        f"({len(base)} reference-made mutants cycled), {n_img} images "
                         "(batch 100) of the 10k-image split",
-            "value": 128 / d, "unit": UNIT, "images_per_s": 128 * n_img / d,
-            "e2e": 128 / w, "fp64_dot_tflops": 2.0 * macs * (n_img // batch) * 128 / d / 1e12,
+            "value": pop / d, "unit": UNIT, "images_per_s": pop * n_img / d,
+            "e2e": pop / w, "fp64_dot_tflops": 2.0 * macs * (n_img // batch) * pop / d / 1e12,
             "ms_per_step": 1e3 * d, "statuses_ok": sum(f.error < 1.0 for f in fits)}
 
 
