@@ -195,3 +195,34 @@ def test_two_rank_run_search_under_install_reproduces_history():
     # each rank evaluated only its strided shard of every call
     assert out[0][3] + out[1][3] == len(data["individuals"])
     assert 0 < out[1][3] <= out[0][3]
+
+
+@pytest.mark.gpu
+def test_nccl_allgather_through_libgevo_single_rank():
+    """libgevo's own NCCL path on the device (gevo_comm_unique_id /
+    gevo_comm_init / gevo_allgather / gevo_comm_destroy; NCCL dlopen'ed on
+    first use): a one-rank communicator returns the records it was given,
+    and all_gather_records over it unpacks them like the torch path.  (The
+    multi-rank exchange itself is covered over gloo above; one GPU per
+    gpurun, no ranks that wait on each other on one device.)"""
+    import torch.distributed as dist
+    from paper_2310_10211_b200 import _lib
+    ctx = _lib.Context(0)
+    try:
+        ctx.comm_init(0, 1, _lib.comm_unique_id())
+        send = np.arange(4 * D.RECORD_FIELDS, dtype=np.int64).reshape(4, D.RECORD_FIELDS)
+        out = ctx.allgather(send, 1)
+        assert out.shape == (1, 4, D.RECORD_FIELDS) and np.array_equal(out[0], send)
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+        try:
+            local = send[:3]
+            recs, counts = D.all_gather_records(local, 5, ctx=ctx)
+            assert counts.tolist() == [3] and np.array_equal(recs[0, :3], local)
+        finally:
+            dist.destroy_process_group()
+        ctx.comm_destroy()
+    finally:
+        ctx.close()
